@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark: single-pass inclusive sum-scan on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric: scan Gelem/s and % of HBM roofline at N = 2^28 (BASELINE.json).
+A step is one inclusive scan of one synthetic array (inputs resident in HBM)
+through the C ABI.  N=1: Int32, N = 2^28 (configs[1]); the other dtypes and
+CUB DeviceScan are reported beside it in ``per_dtype``.  N>1 (torchrun, one
+process per GPU, NCCL): weak scaling, every rank holds a 2^28-element shard
+of one global array and runs reduce -> all-gather(1 scalar) -> scan with carry.
+
+Inputs are 1 GiB (i32/f32) or 2 GiB (i64/f64) per array, larger than the
+126 MB L2, so no L2 flush is needed between steps.
+
+``--impl reference`` times the reference algorithm on the host cores (the C
+restatement of chained_scan on all threads, oracle/lscan_oracle.c) on the
+same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_DEFAULT = 1 << 28
+TOK_NP = {"i32": np.int32, "i64": np.int64, "f32": np.float32, "f64": np.float64}
+METRIC = "scan Gelem/s and % of HBM roofline (N=2^28, 4 dtypes) at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=list(TOK_NP), default="i32")
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="elements per GPU")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the per-dtype / CUB side lines")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def synthetic(n: int, tok: str, seed) -> np.ndarray:
+    """Same recipe as the reference's generate_input (bench.py:77-87)."""
+    rng = np.random.default_rng(seed)
+    dt = np.dtype(TOK_NP[tok])
+    if dt.kind == "i":
+        info = np.iinfo(dt)
+        return rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+    return rng.uniform(-1.0, 1.0, size=n).astype(dt)
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_ burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Polls NVML SM clock and throttle reasons on a thread during the timed region."""
+
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+        0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- ours --
+
+def time_device(fn, steps, warmup, stream, dist=None):
+    """W untimed steps, then exactly K steps between barrier+sync pairs,
+    timed with CUDA events on the launching stream; returns ms/step (max over ranks)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def cub_gelems(tok: str, xd, steps: int, warmup: int):
+    """Side reference: cub::DeviceScan::InclusiveSum on the same buffers."""
+    import ctypes
+
+    import torch
+    path = os.path.join(REPO, "bench_support", "_build", "libcubside.so")
+    if not os.path.exists(path):
+        return None
+    L = ctypes.CDLL(path)
+    L.cub_inclusive_sum.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t), ctypes.c_void_p]
+    code = {"i32": 0, "i64": 1, "f32": 2, "f64": 3}[tok]
+    n = xd.numel()
+    yd = torch.empty_like(xd)
+    tb = ctypes.c_size_t(0)
+    s = torch.cuda.current_stream()
+    assert L.cub_inclusive_sum(code, xd.data_ptr(), yd.data_ptr(), n, None, ctypes.byref(tb), s.cuda_stream) == 0
+    temp = torch.empty(max(tb.value, 1), dtype=torch.uint8, device="cuda")
+
+    def step():
+        rc = L.cub_inclusive_sum(code, xd.data_ptr(), yd.data_ptr(), n, temp.data_ptr(), ctypes.byref(tb),
+                                 s.cuda_stream)
+        assert rc == 0
+
+    ms = time_device(step, steps, warmup, s)
+    return n / (ms * 1e-3) * 1e-9
+
+
+def cpu_reference(tok: str, n: int, samples: int = 3):
+    """The reference algorithm on the host cores: oracle/lscan_oracle.c's
+    threaded restatement of chained_scan (B = all hardware threads,
+    L = 65536 as in test_acceptance.py:281-282), on a bounded sample."""
+    import oracle  # bench's cpu_baseline leg only
+    cores = os.cpu_count() or 1
+    x = synthetic(n, tok, [0, n])
+    y = np.empty_like(x)
+    oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)  # warm
+    ts = []
+    for _ in range(samples):
+        t0 = time.perf_counter()
+        oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)
+        ts.append(time.perf_counter() - t0)
+    seq_t = []
+    xs = x[: min(n, 1 << 24)]
+    for _ in range(2):
+        t0 = time.perf_counter()
+        oracle.sequential_scan(xs)
+        seq_t.append(time.perf_counter() - t0)
+    return {
+        "value": n / min(ts) * 1e-9, "unit": "Gelem/s", "cores": cores, "kind": "port",
+        "sample": f"{tok} N={n} (the bench workload), C restatement of chained_scan, B={cores} threads, "
+                  f"L=65536, best of {samples} ({min(ts):.3f} s)",
+        "numpy_sequential_gelems": xs.size / min(seq_t) * 1e-9,
+        "cpu_model": _cpu_model(),
+    }
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1604_04815_b200 as P
+    from paper_1604_04815_b200 import _native as N
+    from paper_1604_04815_b200 import scan as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    use_dist = world > 1
+    if use_dist:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tok = args.dtype
+    n = args.n
+    tdt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[tok]
+    es = np.dtype(TOK_NP[tok]).itemsize
+    peak, peak_src = peaks()
+
+    # synthetic input: the reference's generator, shard `rank` of the global array
+    xh = synthetic(n, tok, [rank, n])
+    xd = torch.from_numpy(xh).cuda()
+    yd = torch.empty_like(xd)
+    stream = torch.cuda.current_stream()
+
+    if use_dist:
+        from paper_1604_04815_b200.distributed import sharded_scan
+
+        def step():
+            sharded_scan(xd, out=None)
+    else:
+        def step():
+            S.inclusive_scan(xd, out=yd)
+
+    # correctness of the measured configuration (bit-exact ints vs golden digest)
+    validated = None
+    if not use_dist:
+        S.inclusive_scan(xd, out=yd)
+        torch.cuda.synchronize()
+        golden = os.path.join(REPO, "tests", "golden", "digests.json")
+        try:
+            import hashlib
+            cases = json.load(open(golden))["cases"]
+            case = next((c for c in cases if c["n"] == n and c["dtype"] == tok), None)
+            if case is not None and tok[0] == "i":
+                validated = hashlib.sha256(yd.cpu().numpy().tobytes()).hexdigest()[:16] == case["y_sha16"]
+        except Exception:
+            validated = None
+
+    sampler = ClockSampler(local)
+    for _ in range(args.warmup):
+        step()
+    with sampler:
+        ms = time_device(step, args.steps, 0, stream, dist if use_dist else None)
+    # native launches per step, counted through the library's launch counter
+    c0 = N.launch_count()
+    step()
+    torch.cuda.synchronize()
+    per_step = N.launch_count() - c0
+    total_elems = n * world
+    value = total_elems / (ms * 1e-3) * 1e-9
+    # dominant kernel: the scan kernel; at N=1 it is the whole step
+    scan_ms = ms if not use_dist else time_device(lambda: S.inclusive_scan(xd, out=yd), 20, 3, stream, None)
+    alg_bytes = 2 * n * es
+    achieved = alg_bytes / (scan_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(tok, n),
+                "peak_source": peak_src, "kernel": "scan_kernel (lscan::scan_kernel, TMA ring)",
+                "algorithmic_bytes_per_launch": alg_bytes}
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Gelem/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": tok,
+        "data": "synthetic (reference generate_input recipe: full-range ints / U[-1,1] floats, seed [rank, n])",
+        "config": {"workload": f"{tok} inclusive sum-scan, N=2^{n.bit_length() - 1} per GPU"
+                               + (" (BASELINE configs[1])" if n == N_DEFAULT and tok == "i32" else ""),
+                   "n_per_gpu": n, "n_total": total_elems, "op": "add",
+                   "l2": "inputs (>=1 GiB) larger than L2 (126 MB); no flush",
+                   "parallelism": f"shard{world}" if use_dist else "single",
+                   "kernel_geometry": S.query_config(tdt, n)},
+        "roofline": roofline,
+        "gpu_launches": per_step * args.steps,
+        "clocks": sampler.summary(),
+        "validated": validated,
+    }
+
+    # ---- e2e through the public API with host buffers
+    if not args.no_e2e and not use_dist:
+        xp = torch.empty(n, dtype=tdt).pin_memory()
+        yp = torch.empty(n, dtype=tdt).pin_memory()
+        xp.numpy()[:] = xh
+        op = P.make_operator("add", tok)
+        prob = P.ScanProblem(xp.numpy(), op, out=yp.numpy())
+        P.chained_scan(prob)
+        ts = []
+        for _ in range(max(3, min(args.steps, 5))):
+            t0 = time.perf_counter()
+            P.chained_scan(prob)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = statistics.median(ts)
+        out["e2e"] = {"value": round(n / e2e_s * 1e-9, 3), "unit": "Gelem/s",
+                      "h2d_bytes_per_step": n * es, "d2h_bytes_per_step": n * es,
+                      "api": "paper_1604_04815_b200.chained_scan(ScanProblem(pinned numpy x, add, out=pinned y))",
+                      "ms_per_step": round(e2e_s * 1e3, 3)}
+        if tok[0] == "i":
+            out["e2e"]["validated"] = bool(np.array_equal(yp.numpy()[-1000:], yd.cpu().numpy()[-1000:]))
+        del xp, yp
+
+    # ---- the other dtypes and CUB on the same box (N=1 only)
+    if not args.no_sweep and not use_dist:
+        per = {}
+        for t2 in ("i32", "i64", "f32", "f64"):
+            d2 = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[t2]
+            e2 = np.dtype(TOK_NP[t2]).itemsize
+            if t2 == tok:
+                x2, y2 = xd, yd
+            else:
+                x2 = torch.from_numpy(synthetic(n, t2, [0, n])).cuda()
+                y2 = torch.empty_like(x2)
+            ms2 = time_device(lambda: S.inclusive_scan(x2, out=y2), 50, 5, stream)
+            g = n / (ms2 * 1e-3) * 1e-9
+            cub = cub_gelems(t2, x2, 50, 5)
+            per[t2] = {"gelems": round(g, 2), "gbs": round(2 * n * e2 / (ms2 * 1e-3) / 1e9, 1),
+                       "frac_of_measured_hbm": round(2 * n * e2 / (ms2 * 1e-3) / 1e9 / peak, 4),
+                       "frac_of_nominal_8tbs": round(2 * n * e2 / (ms2 * 1e-3) / 1e12 / 8.0, 4),
+                       "cub_gelems": None if cub is None else round(cub, 2)}
+            del x2, y2
+            torch.cuda.empty_cache()
+        out["per_dtype"] = per
+
+    if not args.no_cpu and rank == 0 and not use_dist:
+        out["cpu_baseline"] = cpu_reference(tok, n)
+
+    if use_dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def _ncu_traffic(tok, n):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"{tok}_{n}")
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the reference arm runs on rank 0 only
+    tok, n = args.dtype, args.n
+    steps = max(1, args.steps)
+    warm = max(0, args.warmup)
+    import oracle
+    cores = os.cpu_count() or 1
+    x = synthetic(n, tok, [0, n])
+    y = np.empty_like(x)
+    # bounded: at most ~3 timed samples + 1 warm-up of the full workload
+    k = min(steps, 3)
+    for _ in range(min(warm, 1)):
+        oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)
+    ts = []
+    for _ in range(k):
+        t0 = time.perf_counter()
+        oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    value = n / t * 1e-9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gelem/s",
+        "n_gpus": args.gpus, "steps": k, "warmup": min(warm, 1), "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": tok,
+        "data": "synthetic (reference generate_input recipe)",
+        "config": {"workload": f"{tok} inclusive sum-scan, N=2^{n.bit_length() - 1}", "n_per_gpu": n},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gelem/s", "cores": cores, "kind": "port",
+                         "sample": f"{tok} N={n}, C restatement of chained_scan (oracle/lscan_oracle.c), "
+                                   f"B={cores} threads, L=65536, median of {k}",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": round(value, 4), "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

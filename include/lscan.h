@@ -1,0 +1,117 @@
+/*
+ * lscan.h — C ABI of the B200-native single-pass sum-scan (LightScan,
+ * arXiv 1604.04815) that replaces the reference's scan entry point.
+ *
+ * Reference interface replaced (chainscan 0.1.0, Python):
+ *   chained_scan(problem: ScanProblem, config=None) -> ndarray
+ *       /root/reference/pkg/src/chainscan/chained.py:316-357
+ *   run_algorithm("chained", problem, chain_config)   bench.py:121-147 (:333-334 in file)
+ *   ScanProblem (x, op, out; out may alias x)          reference.py:38-58
+ *   make_operator("add", i32|i64|f32|f64)              operators.py:111-127
+ *   LivenessError / ProtocolViolation                  chained.py:48-53
+ *   ChainConfig.spin_budget / corrupt_slot             chained.py:222-224
+ *
+ * Conventions: plain pointers and sizes only; device pointers are owned by
+ * the caller; every device call is stream-ordered and asynchronous (the
+ * stream is a cudaStream_t passed as void*, NULL = legacy default stream).
+ * Inputs must be 1-D contiguous arrays of the element type; x == y (in
+ * place) is allowed, any other overlap of x and y is rejected.  Integer sums
+ * wrap modulo 2^width (two's complement), exactly like the reference's
+ * np.add under errstate(over="ignore") (operators.py:74-100).
+ *
+ * Errors are status codes; ls_last_error_detail() returns a thread-local
+ * message for the last failing call on the calling thread.
+ */
+#ifndef LSCAN_H
+#define LSCAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LS_OK = 0,
+    LS_ERR_INVALID_ARG = 1,       /* ShapeError / ValueError (reference.py:50-55, chained.py:227-234) */
+    LS_ERR_UNSUPPORTED_DTYPE = 2, /* UnsupportedOperatorError (operators.py:34-47) */
+    LS_ERR_CUDA = 3,              /* a CUDA runtime call failed */
+    LS_ERR_LIVENESS = 4,          /* LivenessError: debug spin budget exhausted (chained.py:139-144) */
+    LS_ERR_PROTOCOL = 5,          /* ProtocolViolation: slot published twice (chained.py:117-118) */
+    LS_ERR_WORKSPACE = 6          /* workspace missing / too small / not initialised */
+} ls_status;
+
+typedef enum { LS_I32 = 0, LS_I64 = 1, LS_F32 = 2, LS_F64 = 3 } ls_dtype;
+
+/* ---- workspace ------------------------------------------------------------
+ * The carry-chain buffer (the reference's CommSlots, chained.py:85-150): one
+ * write-once slot per data tile plus one per round, epoch-tagged so a call
+ * never needs a memset.  Size depends on n and the current device.  A fresh
+ * workspace must be zeroed once with ls_workspace_init; after that it can be
+ * reused by any number of calls issued in stream order. */
+size_t ls_workspace_bytes(ls_dtype dt, int64_t n);
+ls_status ls_workspace_init(void *ws, size_t ws_bytes, void *stream);
+
+/* ---- device scans (the hot path) -------------------------------------------
+ * y[j] = carry (+) x[0] (+) ... (+) x[j]            (inclusive)
+ * y[j] = carry (+) x[0] (+) ... (+) x[j-1]          (exclusive; y[0] = carry)
+ * carry_in: nullable device scalar (identity when NULL) — the multi-GPU
+ *   carry from lower shards.
+ * total_out: nullable device scalar receiving carry (+) sum(x).
+ * Replaces chained_scan (chained.py:316) for op "add". */
+ls_status ls_inclusive_sum(ls_dtype dt, const void *x, void *y, int64_t n,
+                           const void *carry_in, void *total_out,
+                           void *ws, size_t ws_bytes, void *stream);
+ls_status ls_exclusive_sum(ls_dtype dt, const void *x, void *y, int64_t n,
+                           const void *carry_in, void *total_out,
+                           void *ws, size_t ws_bytes, void *stream);
+
+/* total_out = sum(x) (device scalar), deterministic for a given device; the
+ * per-shard total of the multi-GPU carry exchange. */
+ls_status ls_reduce_sum(ls_dtype dt, const void *x, int64_t n, void *total_out,
+                        void *ws, size_t ws_bytes, void *stream);
+
+/* carry_out[g] = t[0] (+) ... (+) t[g-1] for g < count (exclusive scan of
+ * the gathered per-rank totals, fixed left-to-right order).
+ * t and carry_out are device arrays of `count` scalars. */
+ls_status ls_carry_from_totals(ls_dtype dt, const void *totals, int64_t count,
+                               int64_t rank, void *carry_out, void *stream);
+
+/* ---- host-buffer entry (what chained_scan(problem) does with numpy arrays) --
+ * x and y are HOST pointers (pinned or pageable; y may equal x).  The array
+ * is streamed through the device in chunks with copy-in, scan and copy-out
+ * overlapped on three streams, the carry chained on the device between
+ * chunks.  Blocks until y is complete.  device < 0 = current device. */
+ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n,
+                                int exclusive, int device);
+
+/* ---- debug hooks (ChainConfig.spin_budget / corrupt_slot, chained.py:222-224)
+ * spin_budget > 0 arms a device watchdog: a look-back that probes a slot more
+ * than spin_budget times records LS_ERR_LIVENESS in the workspace instead of
+ * hanging.  corrupt_block >= 0 makes that tile publish the identity as its
+ * aggregate (fault injection; the output is wrong only after that tile).
+ * With either armed, or protocol_checks != 0, every device call synchronises
+ * its stream and reports the workspace error word as its status.
+ * Process-wide; (0, -1, 0) disarms. */
+ls_status ls_debug_config(int64_t spin_budget, int64_t corrupt_block, int protocol_checks);
+
+/* Reads and clears the device error word of a workspace (synchronises). */
+ls_status ls_workspace_error(void *ws, size_t ws_bytes, void *stream);
+
+/* ---- introspection ---------------------------------------------------------- */
+const char *ls_status_string(ls_status s);
+const char *ls_last_error_detail(void);
+int ls_abi_version(void);
+/* Launch geometry the scan uses on the current device for dt:
+ * out[0] = persistent CTAs (grid), out[1] = threads per CTA, out[2] = elements
+ * per tile, out[3] = pipeline stages, out[4] = resident CTAs per SM,
+ * out[5] = SM count. */
+ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]);
+/* Number of kernel launches this process has issued through the library. */
+int64_t ls_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSCAN_H */

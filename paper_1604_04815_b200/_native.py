@@ -1,0 +1,130 @@
+"""Build and load the native library (``_lib/liblscan.so``) — the C ABI of
+``include/lscan.h`` — through ctypes.
+
+There is no fallback: if the library is missing, was built for another
+architecture, or no CUDA device is visible, every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import List, Optional
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO_DIR = os.path.dirname(PKG_DIR)
+CSRC = os.path.join(PKG_DIR, "csrc")
+INCLUDE = os.path.join(REPO_DIR, "include")
+LIB_DIR = os.path.join(PKG_DIR, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
+
+SOURCES = ["lscan_api.cu", "lscan_host.cu"]
+HEADERS = ["lscan_kernels.cuh", "lscan_ptx.cuh"]
+ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+# ls_status (include/lscan.h)
+LS_OK = 0
+LS_ERR_INVALID_ARG = 1
+LS_ERR_UNSUPPORTED_DTYPE = 2
+LS_ERR_CUDA = 3
+LS_ERR_LIVENESS = 4
+LS_ERR_PROTOCOL = 5
+LS_ERR_WORKSPACE = 6
+
+# ls_dtype
+LS_I32, LS_I64, LS_F32, LS_F64 = 0, 1, 2, 3
+
+EXPORTED = [
+    "ls_workspace_bytes", "ls_workspace_init", "ls_inclusive_sum", "ls_exclusive_sum",
+    "ls_reduce_sum", "ls_carry_from_totals", "ls_inclusive_sum_host", "ls_debug_config",
+    "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
+    "ls_query_config", "ls_launch_count",
+]
+
+
+def _inputs() -> List[str]:
+    return ([os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+            + [os.path.join(INCLUDE, "lscan.h")])
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    return any(os.path.getmtime(p) > t for p in _inputs())
+
+
+def build(force: bool = False, verbose: bool = False, extra: Optional[List[str]] = None) -> str:
+    """nvcc the CUDA sources into ``_lib/liblscan.so`` for sm_100a."""
+    if not force and not needs_build():
+        return LIB_PATH
+    os.makedirs(LIB_DIR, exist_ok=True)
+    nvcc = os.environ.get("NVCC", "nvcc")
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, "-O3", "-std=c++17", *ARCH_FLAGS, "-lineinfo", "-Xcompiler", "-fPIC",
+           "-shared", f"-I{INCLUDE}", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    if extra:
+        cmd[1:1] = extra
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """The loaded library; raises if it is absent (no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"native library {LIB_PATH} is missing; run __graft_entry__.build() "
+                "(or python -c 'import paper_1604_04815_b200._native as n; n.build()')")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, sz, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.c_int
+        sig = {
+            "ls_workspace_bytes": (sz, [ci, i64]),
+            "ls_workspace_init": (ci, [vp, sz, vp]),
+            "ls_inclusive_sum": (ci, [ci, vp, vp, i64, vp, vp, vp, sz, vp]),
+            "ls_exclusive_sum": (ci, [ci, vp, vp, i64, vp, vp, vp, sz, vp]),
+            "ls_reduce_sum": (ci, [ci, vp, i64, vp, vp, sz, vp]),
+            "ls_carry_from_totals": (ci, [ci, vp, i64, i64, vp, vp]),
+            "ls_inclusive_sum_host": (ci, [ci, vp, vp, i64, ci, ci]),
+            "ls_debug_config": (ci, [i64, i64, ci]),
+            "ls_workspace_error": (ci, [vp, sz, vp]),
+            "ls_status_string": (ctypes.c_char_p, [ci]),
+            "ls_last_error_detail": (ctypes.c_char_p, []),
+            "ls_abi_version": (ci, []),
+            "ls_query_config": (ci, [ci, i64, ctypes.POINTER(ctypes.c_int64)]),
+            "ls_launch_count": (i64, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.ls_abi_version() != 1:
+            raise RuntimeError("liblscan ABI version mismatch")
+        _lib = L
+        return _lib
+
+
+def status_string(code: int) -> str:
+    return lib().ls_status_string(code).decode()
+
+
+def last_detail() -> str:
+    return (lib().ls_last_error_detail() or b"").decode(errors="replace")
+
+
+def launch_count() -> int:
+    return int(lib().ls_launch_count())

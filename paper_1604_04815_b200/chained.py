@@ -1,0 +1,169 @@
+"""Drop-in for the reference scan entry point, on the GPU.
+
+``chained_scan(problem, config=None) -> np.ndarray`` keeps the exact
+signature and contract of chainscan's ``chained_scan`` (chained.py:316-357):
+
+* ``problem`` is a ``ScanProblem`` (this package's or the reference's own —
+  only ``x``, ``op`` and ``out`` are read); ``op.name`` must be ``"add"``;
+* the result lands in ``problem.out`` when given (it may alias ``x``, an
+  in-place scan) or in a fresh array, and that array object is returned;
+* ``n == 0`` returns the (empty) output untouched;
+* integers wrap (two's complement) and are bit-identical to the sequential
+  oracle; floats match it within the reference envelope
+  ``1e-5 / 1e-12 * cumsum|x|`` (bench.py:49, :90-114).
+
+The scan runs on the device through the C ABI (``ls_inclusive_sum_host``):
+the host array is streamed through the GPU in chunks with copy-in, scan and
+copy-out overlapped.  There is no CPU path.
+
+``ChainConfig`` keeps the reference's fields (chained.py:205-234).  On the
+GPU, ``b`` (workers) and ``geometry`` (block shape) are decided by the
+device (persistent CTAs = co-resident capacity, compile-time tiles) and are
+accepted for compatibility; ``spin_budget``, ``corrupt_slot`` and
+``protocol_checks`` map onto the device watchdog / fault injection /
+publish-once check and raise the reference's ``LivenessError`` /
+``ProtocolViolation``; ``on_block`` (a per-block host callback) has no
+device equivalent and is rejected.
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as N
+from .errors import LivenessError, ProtocolViolation, raise_for_status  # noqa: F401
+from .operators import DTYPES, require_device_operator
+from .problem import ScanProblem, ShapeError
+
+BLOCK_SCAN_MODES = ("vectorized", "warp-model")
+ALGORITHMS = ("chained",)
+
+NP_DT = {np.dtype(np.int32): N.LS_I32, np.dtype(np.int64): N.LS_I64,
+         np.dtype(np.float32): N.LS_F32, np.dtype(np.float64): N.LS_F64}
+
+
+@dataclass(frozen=True)
+class SpinPolicy:
+    """chained.py:60-82.  The device look-back always spins with a short
+    ``nanosleep`` back-off; the policy is validated and kept for parity."""
+
+    kind: str = "spin-yield"
+    yield_threshold: int = 1024
+
+    def __post_init__(self):
+        if self.kind not in ("spin", "spin-yield"):
+            raise ValueError(f"unknown spin policy {self.kind!r}")
+        if self.yield_threshold < 1:
+            raise ValueError("yield threshold must be >= 1")
+
+    @classmethod
+    def spin_then_yield(cls, threshold: int = 1024) -> "SpinPolicy":
+        return cls(kind="spin-yield", yield_threshold=threshold)
+
+
+def default_worker_count() -> int:
+    return os.cpu_count() or 1
+
+
+@dataclass
+class ChainConfig:
+    """chained.py:205-234 (see module docstring for the GPU meaning)."""
+
+    b: int = field(default_factory=default_worker_count)
+    geometry: Optional[object] = None
+    spin: SpinPolicy = field(default_factory=SpinPolicy)
+    block_scan_mode: str = "vectorized"
+    spin_budget: Optional[int] = None
+    protocol_checks: bool = True
+    corrupt_slot: Optional[int] = None
+    on_block: Optional[Callable[[int, int], None]] = None
+
+    def __post_init__(self):
+        if self.b < 1:
+            raise ValueError(f"worker count must be >= 1, got {self.b}")
+        if self.block_scan_mode not in BLOCK_SCAN_MODES:
+            raise ValueError(f"unknown block scan mode {self.block_scan_mode!r}; "
+                             f"choose from {BLOCK_SCAN_MODES}")
+
+
+_debug_lock = threading.Lock()
+
+
+def _device_debug_scan(x: np.ndarray, out: np.ndarray, config: ChainConfig, exclusive: bool) -> None:
+    """One device launch over the whole array with the debug hooks armed
+    (so that ``corrupt_slot`` names a tile of this array, not of a chunk)."""
+    import torch
+
+    from . import scan as S
+    with _debug_lock:
+        raise_for_status(N.lib().ls_debug_config(int(config.spin_budget or 0),
+                                                 -1 if config.corrupt_slot is None else int(config.corrupt_slot),
+                                                 0))
+        try:
+            xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+            yd = S.exclusive_scan(xd) if exclusive else S.inclusive_scan(xd)
+            out[...] = yd.cpu().numpy()
+        finally:
+            N.lib().ls_debug_config(0, -1, 0)
+
+
+def _scan_host(problem, config: Optional[ChainConfig], exclusive: bool) -> np.ndarray:
+    op = problem.op
+    dtype = require_device_operator(op)
+    x = problem.x
+    if x.ndim != 1:
+        raise ShapeError(f"input must be 1-D, got shape {x.shape}")
+    if x.dtype != dtype:
+        # the reference silently computes in x's dtype; the drop-in refuses
+        # the mismatch instead of guessing
+        raise ShapeError(f"input dtype {x.dtype} does not match operator dtype {dtype}")
+    out = problem.out if problem.out is not None else np.empty_like(x)
+    if out.shape != x.shape or out.dtype != dtype:
+        raise ShapeError("out must match the input's shape and dtype")
+    if not out.flags.c_contiguous or not out.flags.writeable:
+        raise ShapeError("out must be a writeable C-contiguous array")
+    n = x.size
+    if n == 0:
+        return out
+    if config is not None and config.on_block is not None:
+        raise ValueError("ChainConfig.on_block is a per-block host callback; the device scan has none")
+    if not x.flags.c_contiguous:
+        x = np.ascontiguousarray(x)
+    if config is not None and (config.spin_budget or config.corrupt_slot is not None):
+        _device_debug_scan(x, out, config, exclusive)
+        return out
+    aliased = problem.out is not None and np.shares_memory(out, x)
+    if aliased and out.ctypes.data != x.ctypes.data:
+        raise ShapeError("out overlaps x without being the same array (only exact in-place is supported)")
+    rc = N.lib().ls_inclusive_sum_host(NP_DT[dtype], x.ctypes.data, out.ctypes.data, n,
+                                       1 if exclusive else 0, -1)
+    raise_for_status(rc)
+    return out
+
+
+def chained_scan(problem: ScanProblem, config: Optional[ChainConfig] = None) -> np.ndarray:
+    """Inclusive sum-scan of ``problem.x`` on the GPU (chained.py:316-357)."""
+    return _scan_host(problem, config, exclusive=False)
+
+
+def chained_exclusive_scan(problem: ScanProblem, config: Optional[ChainConfig] = None) -> np.ndarray:
+    """Exclusive variant (derived mode): y[0] = 0, y[j] = x[0] + ... + x[j-1]."""
+    return _scan_host(problem, config, exclusive=True)
+
+
+def run_algorithm(name: str, problem: ScanProblem, chain_config: Optional[ChainConfig] = None,
+                  rows: Optional[int] = None) -> np.ndarray:
+    """bench.py:121-147 dispatch, restricted to the algorithm this package
+    provides on the device ("chained")."""
+    if name == "chained":
+        return chained_scan(problem, chain_config)
+    raise ValueError(f"unknown algorithm {name!r}; this package provides {ALGORITHMS}")
+
+
+__all__ = ["ChainConfig", "SpinPolicy", "chained_scan", "chained_exclusive_scan", "run_algorithm",
+           "default_worker_count", "BLOCK_SCAN_MODES", "ALGORITHMS", "DTYPES"]

@@ -1,0 +1,176 @@
+"""Device-level API on torch CUDA tensors (the B200 hot path).
+
+``inclusive_scan`` / ``exclusive_scan`` / ``reduce_sum`` call the C ABI of
+``include/lscan.h`` with raw device pointers and the current CUDA stream;
+torch is only the allocator and stream plumbing.  Each (device, stream) keeps
+one workspace (the carry-chain slot buffer), zeroed once and then reused
+across calls through its epoch tags.
+
+Reference counterpart: ``chained_scan`` (chainscan/chained.py:316-357) with
+op ``add``; the numpy-level drop-in with the reference's exact signature is
+``paper_1604_04815_b200.chained.chained_scan``.
+"""
+
+from __future__ import annotations
+
+import threading
+from typing import Dict, Optional, Tuple
+
+import torch
+
+from . import _native as N
+from .errors import raise_for_status
+from .operators import UnsupportedOperatorError
+from .problem import ShapeError
+
+TORCH_DT = {
+    torch.int32: N.LS_I32,
+    torch.int64: N.LS_I64,
+    torch.float32: N.LS_F32,
+    torch.float64: N.LS_F64,
+}
+
+_ws_lock = threading.Lock()
+_workspaces: Dict[Tuple[int, int], torch.Tensor] = {}
+
+
+def dtype_code(dtype: torch.dtype) -> int:
+    try:
+        return TORCH_DT[dtype]
+    except KeyError:
+        raise UnsupportedOperatorError(
+            f"unsupported element type {dtype}; supported: int32, int64, float32, float64") from None
+
+
+def workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> torch.Tensor:
+    """The (device, stream)'s workspace, grown (and zeroed) on demand."""
+    key = (device.index, stream.cuda_stream)
+    with _ws_lock:
+        ws = _workspaces.get(key)
+        if ws is None or ws.numel() < nbytes:
+            size = max(nbytes, 1 << 20)
+            if ws is not None:
+                size = max(size, 2 * ws.numel())
+            with torch.cuda.stream(stream):
+                ws = torch.empty(size + 128, dtype=torch.uint8, device=device)
+                # 128-byte alignment of the header line
+                off = (-ws.data_ptr()) % 128
+                ws = ws[off:off + size]
+                raise_for_status(N.lib().ls_workspace_init(ws.data_ptr(), ws.numel(), stream.cuda_stream))
+            _workspaces[key] = ws
+        return ws
+
+
+def _check_1d(x: torch.Tensor, what: str = "input") -> None:
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"{what} must be a torch.Tensor")
+    if x.dim() != 1:
+        raise ShapeError(f"{what} must be 1-D, got shape {tuple(x.shape)}")
+    if not x.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (there is no CPU path)")
+
+
+def _scalar_ptr(t: Optional[torch.Tensor], like: torch.Tensor, what: str) -> Optional[int]:
+    if t is None:
+        return None
+    if t.device != like.device or t.dtype != like.dtype or t.numel() < 1:
+        raise ValueError(f"{what} must be a device tensor of {like.dtype} on {like.device}")
+    return t.data_ptr()
+
+
+def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exclusive: bool) -> torch.Tensor:
+    _check_1d(x)
+    dt = dtype_code(x.dtype)
+    if out is None:
+        out = torch.empty_like(x, memory_format=torch.contiguous_format)
+    else:
+        _check_1d(out, "out")
+        if out.shape != x.shape:
+            raise ShapeError("out shape must match input shape")
+        if out.dtype != x.dtype or out.device != x.device:
+            raise ValueError("out must have the input's dtype and device")
+        if not out.is_contiguous():
+            raise ShapeError("out must be contiguous")
+    if not x.is_contiguous():
+        x = x.contiguous()
+    n = x.numel()
+    stream = torch.cuda.current_stream(x.device)
+    L = N.lib()
+    ws = workspace(x.device, stream, L.ls_workspace_bytes(dt, n))
+    fn = L.ls_exclusive_sum if exclusive else L.ls_inclusive_sum
+    with torch.cuda.device(x.device):
+        rc = fn(dt, x.data_ptr() if n else None, out.data_ptr() if n else None, n,
+                _scalar_ptr(carry_in, x, "carry_in"), _scalar_ptr(total_out, x, "total_out"),
+                ws.data_ptr(), ws.numel(), stream.cuda_stream)
+    raise_for_status(rc)
+    return out
+
+
+def inclusive_scan(x: torch.Tensor, out: Optional[torch.Tensor] = None, *,
+                   carry_in: Optional[torch.Tensor] = None,
+                   total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y[j] = carry (+) x[0] (+) ... (+) x[j] on the device; ``out`` may be ``x``.
+
+    ``carry_in`` / ``total_out`` are optional one-element device tensors of
+    x's dtype (the multi-GPU carry seam)."""
+    return _scan(x, out, carry_in, total_out, exclusive=False)
+
+
+def exclusive_scan(x: torch.Tensor, out: Optional[torch.Tensor] = None, *,
+                   carry_in: Optional[torch.Tensor] = None,
+                   total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y[0] = carry (identity), y[j] = carry (+) x[0] (+) ... (+) x[j-1]."""
+    return _scan(x, out, carry_in, total_out, exclusive=True)
+
+
+def reduce_sum(x: torch.Tensor, total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Deterministic device sum of x into a one-element tensor."""
+    _check_1d(x)
+    dt = dtype_code(x.dtype)
+    if not x.is_contiguous():
+        x = x.contiguous()
+    if total_out is None:
+        total_out = torch.empty(1, dtype=x.dtype, device=x.device)
+    stream = torch.cuda.current_stream(x.device)
+    L = N.lib()
+    ws = workspace(x.device, stream, L.ls_workspace_bytes(dt, 0))
+    with torch.cuda.device(x.device):
+        rc = L.ls_reduce_sum(dt, x.data_ptr() if x.numel() else None, x.numel(),
+                             _scalar_ptr(total_out, x, "total_out"), ws.data_ptr(), ws.numel(),
+                             stream.cuda_stream)
+    raise_for_status(rc)
+    return total_out
+
+
+def carry_from_totals(totals: torch.Tensor, rank: int, carry_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """carry = totals[0] (+) ... (+) totals[rank-1] on the device (fixed order)."""
+    _check_1d(totals, "totals")
+    dt = dtype_code(totals.dtype)
+    if carry_out is None:
+        carry_out = torch.empty(1, dtype=totals.dtype, device=totals.device)
+    stream = torch.cuda.current_stream(totals.device)
+    with torch.cuda.device(totals.device):
+        rc = N.lib().ls_carry_from_totals(dt, totals.data_ptr(), totals.numel(), rank,
+                                         carry_out.data_ptr(), stream.cuda_stream)
+    raise_for_status(rc)
+    return carry_out
+
+
+def query_config(dtype: torch.dtype, n: int) -> dict:
+    """Launch geometry the scan uses for (dtype, n) on the current device."""
+    import ctypes
+    out = (ctypes.c_int64 * 6)()
+    raise_for_status(N.lib().ls_query_config(dtype_code(dtype), n, out))
+    keys = ("grid", "threads", "tile_elems", "stages", "ctas_per_sm", "sms")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
+def check_workspace_error(device: Optional[torch.device] = None) -> None:
+    """Raise the first device-side error (liveness / protocol) recorded in the
+    current stream's workspace, if any (synchronises)."""
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(device)
+    ws = _workspaces.get((device.index, stream.cuda_stream))
+    if ws is None:
+        return
+    raise_for_status(N.lib().ls_workspace_error(ws.data_ptr(), ws.numel(), stream.cuda_stream))

@@ -1,0 +1,116 @@
+"""The numpy drop-in ``chained_scan(problem, config)`` on the device,
+replaying the shape of the reference's own chained tests
+(test_chained.py, test_acceptance.py C1/C2/C6/C7) against the oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1604_04815_b200 as P  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+
+
+def test_c1_oracle_equivalence_integers(oracle_lib):
+    # test_acceptance.py:55-82 for op add: N sweep x seeds, bit-exact
+    ns = (0, 1, 2, 3, 7, 8, 31, 32, 33, 1024, 100_000, 1_000_000)
+    for tok in ("i32", "i64"):
+        op = P.make_operator("add", tok)
+        for seed in range(5):
+            for n in ns:
+                x = oracle_lib.generate_input(n, tok, [seed, n])
+                y = P.chained_scan(P.ScanProblem(x, op))
+                assert np.array_equal(y, oracle_lib.sequential_scan(x)), (tok, seed, n)
+
+
+def test_c2_float_envelope(oracle_lib):
+    # test_acceptance.py:85-111: N = 1e6, within eps_rel * running |x| sum
+    n = 1_000_000
+    for tok in ("f32", "f64"):
+        op = P.make_operator("add", tok)
+        x = oracle_lib.generate_input(n, tok, [7, n])
+        y = P.chained_scan(P.ScanProblem(x, op))
+        assert oracle_lib.validate_output(x, y) is None
+
+
+def test_c7_in_place_and_returns_out(oracle_lib):
+    # test_acceptance.py:246-262, test_chained.py:185-192
+    op = P.make_operator("add", "i64")
+    for trial in range(5):
+        x = oracle_lib.generate_input(100_000, "i64", [trial, 77])
+        want = P.chained_scan(P.ScanProblem(x, op))
+        buf = x.copy()
+        got = P.chained_scan(P.ScanProblem(buf, op, out=buf))
+        assert got is buf and np.array_equal(buf, want)
+    out = np.empty(1000, dtype=np.int64)
+    x = oracle_lib.generate_input(1000, "i64", 1)
+    assert P.chained_scan(P.ScanProblem(x, op, out=out)) is out
+
+
+def test_multi_chunk_host_pipeline(oracle_lib):
+    # > one 64 MiB device chunk: the carry crosses chunk launches
+    n = 40_000_003
+    for tok in ("i32", "f64"):
+        op = P.make_operator("add", tok)
+        x = oracle_lib.generate_input(n, tok, [1, n])
+        y = P.chained_scan(P.ScanProblem(x, op))
+        if tok == "i32":
+            assert np.array_equal(y, oracle_lib.c_sequential_scan(x)[0])
+        else:
+            assert oracle_lib.validate_output(x, y, ref=oracle_lib.c_sequential_scan(x)[0]) is None
+        ye = P.chained_exclusive_scan(P.ScanProblem(x, op))
+        if tok == "i32":
+            assert np.array_equal(ye, oracle_lib.c_sequential_scan(x, exclusive=True)[0])
+
+
+def test_pinned_host_buffers(oracle_lib):
+    n = 20_000_001
+    x = oracle_lib.generate_input(n, "i32", [2, n])
+    xp = torch.empty(n, dtype=torch.int32).pin_memory()
+    yp = torch.empty(n, dtype=torch.int32).pin_memory()
+    xp.numpy()[:] = x
+    y = P.chained_scan(P.ScanProblem(xp.numpy(), P.make_operator("add", "i32"), out=yp.numpy()))
+    assert np.array_equal(y, oracle_lib.c_sequential_scan(x)[0])
+
+
+def test_corrupt_slot_breaks_only_downstream(oracle_lib):
+    # test_chained.py:275-284 on the device: tile 1 publishes the identity
+    cfg_q = P.query_config(torch.int64, 1 << 20)
+    T = cfg_q["tile_elems"]
+    x = np.ones(T * 4, dtype=np.int64)
+    op = P.make_operator("add", "i64")
+    good = P.chained_scan(P.ScanProblem(x, op))
+    bad = P.chained_scan(P.ScanProblem(x, op), P.ChainConfig(corrupt_slot=1))
+    assert np.array_equal(good, oracle_lib.sequential_scan(x))
+    assert not np.array_equal(bad, good)
+    assert np.array_equal(bad[:2 * T], good[:2 * T])
+
+
+def test_spin_budget_armed_does_not_fire_on_healthy_runs(oracle_lib):
+    op = P.make_operator("add", "i32")
+    x = oracle_lib.generate_input(3_000_000, "i32", [1, 1])
+    y = P.chained_scan(P.ScanProblem(x, op), P.ChainConfig(spin_budget=50_000_000))
+    assert np.array_equal(y, oracle_lib.sequential_scan(x))
+
+
+def test_c6_worker_count_is_irrelevant(oracle_lib):
+    # test_acceptance.py:226-243: integer output identical for any B
+    op = P.make_operator("add", "i32")
+    x = oracle_lib.generate_input(100_000, "i32", [0, 61])
+    outs = [P.chained_scan(P.ScanProblem(x, op), P.ChainConfig(b=b)) for b in (1, 2, 4, 8, 16)]
+    for y in outs[1:]:
+        assert np.array_equal(outs[0], y)
+
+
+def test_on_block_hook_rejected():
+    op = P.make_operator("add", "i32")
+    with pytest.raises(ValueError):
+        P.chained_scan(P.ScanProblem(np.ones(10, dtype=np.int32), op),
+                       P.ChainConfig(on_block=lambda w, b: None))
