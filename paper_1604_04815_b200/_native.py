@@ -20,7 +20,7 @@ INCLUDE = os.path.join(REPO_DIR, "include")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
 
-SOURCES = ["lscan_api.cu", "lscan_host.cu"]
+SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_lab.cu"]
 HEADERS = ["lscan_kernels.cuh", "lscan_ptx.cuh"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

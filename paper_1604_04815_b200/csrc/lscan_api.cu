@@ -18,6 +18,7 @@
 
 #include "lscan.h"
 #include "lscan_kernels.cuh"
+#include "lscan_scan_ws.cuh"
 
 using namespace lscan;
 
@@ -29,11 +30,17 @@ void set_detail(const std::string &msg) { g_detail = msg; }
 namespace {
 
 // ---------------------------------------------------------------- tuning --
-// One 32 KiB tile of x per CTA iteration, 512 threads (64 B per thread),
-// six-deep TMA ring (192 KiB of shared memory) -> one CTA per SM, 148 CTAs.
-constexpr int kThreads = 512;
+// Hot path (16-byte aligned x and y): the warp-specialised kernel — 16
+// scanner warps + producer + reducer + look-back warps, one 32 KiB tile of x
+// per iteration, six-deep TMA ring (192 KiB smem) -> one CTA per SM.
+// Generic path (any element alignment): the sequential kernel with plain
+// loads/stores through a two-tile staging buffer.
+constexpr int kScanWarps = 16;
+constexpr int kWsThreads = (kScanWarps + 3) * 32;
 constexpr int kTileBytes = 32768;
 constexpr int kStages = 6;
+constexpr int kThreads = 512;  // generic path
+constexpr int kGenStages = 2;
 constexpr int kReduceThreads = 512;
 
 std::atomic<int64_t> g_launches{0};
@@ -83,32 +90,41 @@ int elem_size(ls_dtype dt) {
 int64_t tile_elems(ls_dtype dt) { return kTileBytes / elem_size(dt); }
 int64_t num_tiles(ls_dtype dt, int64_t n) { return (n + tile_elems(dt) - 1) / tile_elems(dt); }
 
-size_t smem_bytes(int es) {
-    return (size_t)kStages * kTileBytes + (size_t)kStages * 8 + (size_t)(2 * (kThreads / 32) + 1) * es + 16;
+template <typename T>
+size_t ws_smem() { return scan_ws_smem_bytes<T, kScanWarps, kTileBytes, kStages>(); }
+
+size_t gen_smem(int es) {
+    return (size_t)kGenStages * kTileBytes + (size_t)kGenStages * 8 + (size_t)(2 * (kThreads / 32) + 1) * es + 16;
 }
 
 // ----------------------------------------------------- kernel dispatch --
 using ScanFn = void (*)(const ScanParams);
 
-template <typename T, bool EXCL, bool TMA>
-ScanFn scan_fn() {
-    return &scan_kernel<T, kThreads, kTileBytes, kStages, EXCL, TMA>;
-}
+struct Launch {
+    ScanFn fn;
+    int threads;
+    size_t smem;
+};
 
 template <typename T>
-ScanFn pick_typed(bool excl, bool tma) {
-    if (excl) return tma ? scan_fn<T, true, true>() : scan_fn<T, true, false>();
-    return tma ? scan_fn<T, false, true>() : scan_fn<T, false, false>();
+Launch pick_typed(bool excl, bool fast) {
+    if (fast)
+        return {excl ? &scan_ws_kernel<T, kScanWarps, kTileBytes, kStages, true>
+                     : &scan_ws_kernel<T, kScanWarps, kTileBytes, kStages, false>,
+                kWsThreads, ws_smem<T>()};
+    return {excl ? &scan_kernel<T, kThreads, kTileBytes, kGenStages, true, false>
+                 : &scan_kernel<T, kThreads, kTileBytes, kGenStages, false, false>,
+            kThreads, gen_smem(sizeof(T))};
 }
 
-ScanFn pick_scan(ls_dtype dt, bool excl, bool tma) {
+Launch pick_scan(ls_dtype dt, bool excl, bool fast) {
     switch (dt) {
-    case LS_I32: return pick_typed<uint32_t>(excl, tma);
-    case LS_I64: return pick_typed<uint64_t>(excl, tma);
-    case LS_F32: return pick_typed<float>(excl, tma);
-    case LS_F64: return pick_typed<double>(excl, tma);
+    case LS_I32: return pick_typed<uint32_t>(excl, fast);
+    case LS_I64: return pick_typed<uint64_t>(excl, fast);
+    case LS_F32: return pick_typed<float>(excl, fast);
+    case LS_F64: return pick_typed<double>(excl, fast);
     }
-    return nullptr;
+    return {nullptr, 0, 0};
 }
 
 struct DevState {
@@ -130,17 +146,16 @@ ls_status device_state(DevState **out) {
     if (!d.init) {
         LS_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
         for (int dt = 0; dt < 4; ++dt) {
-            const size_t sm = smem_bytes(elem_size((ls_dtype)dt));
             for (int ex = 0; ex < 2; ++ex)
                 for (int tm = 0; tm < 2; ++tm) {
-                    ScanFn f = pick_scan((ls_dtype)dt, ex != 0, tm != 0);
-                    LS_CUDA(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sm),
+                    const Launch L = pick_scan((ls_dtype)dt, ex != 0, tm != 0);
+                    LS_CUDA(cudaFuncSetAttribute((const void *)L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)L.smem),
                             "cudaFuncSetAttribute(max dynamic smem)");
                     int occ = 0;
-                    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)f, kThreads, sm),
+                    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)L.fn, L.threads, L.smem),
                             "occupancy query");
-                    if (occ < 1) return fail(LS_ERR_CUDA, "scan kernel cannot be resident (smem %zu B)", sm);
+                    if (occ < 1) return fail(LS_ERR_CUDA, "scan kernel cannot be resident (smem %zu B)", L.smem);
                     d.occ[dt][ex][tm] = occ;
                 }
         }
@@ -244,22 +259,23 @@ ls_status scan_impl(ls_dtype dt, const void *x, void *y, int64_t n, const void *
     p.spin_budget = dbg.spin_budget;
     p.corrupt_tile = dbg.corrupt;
     p.protocol_checks = dbg.protocol;
+    p.experiment = 0;
 
     // Cooperative launch: the driver refuses a grid that cannot be fully
     // co-resident, which is the deadlock-freedom precondition of the
     // persistent chain (chainscan/schedsim.py's invariant).
     cudaLaunchConfig_t cfg = {};
+    const Launch L = pick_scan(dt, excl, tma);
     cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem_bytes(es);
+    cfg.blockDim = dim3((unsigned)L.threads);
+    cfg.dynamicSmemBytes = L.smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    ScanFn f = pick_scan(dt, excl, tma);
-    LS_CUDA(cudaLaunchKernelEx(&cfg, f, p), "scan kernel launch");
+    LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "scan kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (dbg.armed()) return read_device_error(ws, s, true);
     return LS_OK;
@@ -387,7 +403,7 @@ ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]) {
     const int occ = d->occ[dt][0][1];
     const int64_t M = num_tiles(dt, n);
     out[0] = std::min<int64_t>(std::max<int64_t>(M, 1), (int64_t)occ * d->sms);
-    out[1] = kThreads;
+    out[1] = kWsThreads;
     out[2] = tile_elems(dt);
     out[3] = kStages;
     out[4] = occ;

@@ -96,6 +96,7 @@ struct ScanParams {
     int64_t spin_budget;    // 0 = unlimited
     int64_t corrupt_tile;   // -1 = off
     int protocol_checks;
+    int experiment;         // lab-only bits: 1 = skip the look-back (timing upper bound, wrong sums)
 };
 
 template <typename T>
@@ -399,8 +400,10 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const ScanParams p) {
                 }
                 S::publish(agg, t, tag, t == p.corrupt_tile ? T(0) : tile_agg);
             }
-            T prefix;
-            const bool has = round_lookback<T>(agg, rnd, k, c, G, tag, carry_in, lane, p.spin_budget, hdr, prefix);
+            T prefix = T(0);
+            const bool has = (p.experiment & 1)
+                                 ? false
+                                 : round_lookback<T>(agg, rnd, k, c, G, tag, carry_in, lane, p.spin_budget, hdr, prefix);
             const T incl = has ? (prefix + tile_agg) : tile_agg;
             if (lane == 0) {
                 if (c == G - 1 && t + 1 < M) S::publish(rnd, k, tag, incl);
