@@ -25,7 +25,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -71,63 +70,73 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+_SAMPLER = r"""
+import sys, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        print(time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except Exception:
+        pass
+    time.sleep(0.004)
+"""
+
+
 class ClockSampler:
-    """Polls NVML SM clock and throttle reasons on a thread during the timed region."""
+    """Samples NVML SM clock and clock-event (throttle) reasons from a separate
+    process every ~4 ms; only samples inside [start, stop] of the timed region
+    are kept."""
 
     REASONS = {
-        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
-        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
-        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
-        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
-        0x0000000000000100: "display_clock_setting",
+        0x0000000000000002: "applications_clocks_setting", 0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown", 0x0000000000000010: "sync_boost",
+        0x0000000000000020: "sw_thermal_slowdown", 0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown", 0x0000000000000100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.005):
-        self.index, self.period = index, period_s
-        self.samples, self.reasons = [], set()
+    def __init__(self, index: int):
+        import subprocess
+        self.proc = None
         self.max_mhz = None
-        self._stop = threading.Event()
-        self._t = None
-        self.ok = False
+        self.t0 = self.t1 = None
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception as e:  # pragma: no cover - no NVML
-            self.err = str(e)
-
-    def _run(self):
-        nv = self.nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()
+            self.max_mhz = int(first[1]) if first and first[0] == "max" else None
+        except Exception:
+            self.proc = None
 
     def __enter__(self):
-        if self.ok:
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join()
+        self.t1 = time.time()
+        time.sleep(0.01)
 
     def summary(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        mhz, reasons = [], set()
+        for line in out.splitlines():
+            parts = line.split()
+            if len(parts) != 3:
+                continue
+            t, m, mask = float(parts[0]), int(parts[1]), int(parts[2])
+            if self.t0 is not None and self.t0 <= t <= self.t1:
+                mhz.append(m)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        reasons.add(name)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(mhz)}
 
 
 # --------------------------------------------------------------------- ours --
@@ -283,6 +292,7 @@ def run_ours(args):
         step()
     with sampler:
         ms = time_device(step, args.steps, 0, stream, dist if use_dist else None)
+    clocks = sampler.summary()
     # native launches per step, counted through the library's launch counter
     c0 = N.launch_count()
     step()
@@ -296,7 +306,7 @@ def run_ours(args):
     achieved = alg_bytes / (scan_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(tok, n),
-                "peak_source": peak_src, "kernel": "scan_kernel (lscan::scan_kernel, TMA ring)",
+                "peak_source": peak_src, "kernel": "lscan::scan_ws2_kernel (warp-specialised, TMA ring, register results)",
                 "algorithmic_bytes_per_launch": alg_bytes}
 
     out = {
@@ -312,7 +322,7 @@ def run_ours(args):
                    "kernel_geometry": S.query_config(tdt, n)},
         "roofline": roofline,
         "gpu_launches": per_step * args.steps,
-        "clocks": sampler.summary(),
+        "clocks": clocks,
         "validated": validated,
     }
 

@@ -96,6 +96,16 @@ ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n,
  * Process-wide; (0, -1, 0) disarms. */
 ls_status ls_debug_config(int64_t spin_budget, int64_t corrupt_block, int protocol_checks);
 
+/* Timing perturbation for race testing (the device analogue of the
+ * reference's randomised on_block delays, test_chained.py:239-256): the
+ * reducer warp sleeps reducer_delay_ns on tiles t % 3 == 1 and one scanner
+ * warp sleeps scanner_delay_ns on tiles t % 3 == 2.  Results must not change.
+ * stall_tile >= 0 makes that tile never publish its aggregate — a real stall
+ * of the chain (test_chained.py:259-272); it is honoured only while a spin
+ * budget is armed, so the watchdog turns it into LS_ERR_LIVENESS.
+ * Process-wide; (0, 0, -1) disarms. */
+ls_status ls_debug_perturb(int64_t reducer_delay_ns, int64_t scanner_delay_ns, int64_t stall_tile);
+
 /* Reads and clears the device error word of a workspace (synchronises). */
 ls_status ls_workspace_error(void *ws, size_t ws_bytes, void *stream);
 

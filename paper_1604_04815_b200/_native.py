@@ -21,7 +21,7 @@ LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
 
 SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_lab.cu"]
-HEADERS = ["lscan_kernels.cuh", "lscan_ptx.cuh"]
+HEADERS = ["lscan_kernels.cuh", "lscan_ptx.cuh", "lscan_scan_ws.cuh", "lscan_scan_ws2.cuh"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 # ls_status (include/lscan.h)
@@ -38,7 +38,7 @@ LS_I32, LS_I64, LS_F32, LS_F64 = 0, 1, 2, 3
 
 EXPORTED = [
     "ls_workspace_bytes", "ls_workspace_init", "ls_inclusive_sum", "ls_exclusive_sum",
-    "ls_reduce_sum", "ls_carry_from_totals", "ls_inclusive_sum_host", "ls_debug_config",
+    "ls_reduce_sum", "ls_carry_from_totals", "ls_inclusive_sum_host", "ls_debug_config", "ls_debug_perturb",
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
     "ls_query_config", "ls_launch_count",
 ]
@@ -101,6 +101,7 @@ def lib():
             "ls_carry_from_totals": (ci, [ci, vp, i64, i64, vp, vp]),
             "ls_inclusive_sum_host": (ci, [ci, vp, vp, i64, ci, ci]),
             "ls_debug_config": (ci, [i64, i64, ci]),
+            "ls_debug_perturb": (ci, [i64, i64, i64]),
             "ls_workspace_error": (ci, [vp, sz, vp]),
             "ls_status_string": (ctypes.c_char_p, [ci]),
             "ls_last_error_detail": (ctypes.c_char_p, []),

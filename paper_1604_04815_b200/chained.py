@@ -29,7 +29,6 @@ device equivalent and is rejected.
 from __future__ import annotations
 
 import os
-import threading
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -91,25 +90,17 @@ class ChainConfig:
                              f"choose from {BLOCK_SCAN_MODES}")
 
 
-_debug_lock = threading.Lock()
-
-
 def _device_debug_scan(x: np.ndarray, out: np.ndarray, config: ChainConfig, exclusive: bool) -> None:
     """One device launch over the whole array with the debug hooks armed
     (so that ``corrupt_slot`` names a tile of this array, not of a chunk)."""
     import torch
 
     from . import scan as S
-    with _debug_lock:
-        raise_for_status(N.lib().ls_debug_config(int(config.spin_budget or 0),
-                                                 -1 if config.corrupt_slot is None else int(config.corrupt_slot),
-                                                 0))
-        try:
-            xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
-            yd = S.exclusive_scan(xd) if exclusive else S.inclusive_scan(xd)
-            out[...] = yd.cpu().numpy()
-        finally:
-            N.lib().ls_debug_config(0, -1, 0)
+    with S.debug(spin_budget=int(config.spin_budget or 0),
+                 corrupt_tile=-1 if config.corrupt_slot is None else int(config.corrupt_slot)):
+        xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        yd = S.exclusive_scan(xd) if exclusive else S.inclusive_scan(xd)
+        out[...] = yd.cpu().numpy()
 
 
 def _scan_host(problem, config: Optional[ChainConfig], exclusive: bool) -> np.ndarray:

@@ -18,7 +18,7 @@
 
 #include "lscan.h"
 #include "lscan_kernels.cuh"
-#include "lscan_scan_ws.cuh"
+#include "lscan_scan_ws2.cuh"
 
 using namespace lscan;
 
@@ -30,16 +30,28 @@ void set_detail(const std::string &msg) { g_detail = msg; }
 namespace {
 
 // ---------------------------------------------------------------- tuning --
-// Hot path (16-byte aligned x and y): the warp-specialised kernel — 16
-// scanner warps + producer + reducer + look-back warps, one 32 KiB tile of x
-// per iteration, six-deep TMA ring (192 KiB smem) -> one CTA per SM.
+// Hot path (16-byte aligned x and y): the warp-specialised kernel with
+// register-resident results (scan_ws2_kernel) — 8 scanner warps + producer +
+// reducer + look-back warps, one 32 KiB tile of x per iteration, six-deep TMA
+// ring (192 KiB smem) -> one CTA per SM.  Chosen from the lab sweep in
+// profiles/r1_lab_ws2.json (810 Gelem/s i32, ~99.5% of the measured copy).
 // Generic path (any element alignment): the sequential kernel with plain
 // loads/stores through a two-tile staging buffer.
-constexpr int kScanWarps = 16;
-constexpr int kWsThreads = (kScanWarps + 3) * 32;
-constexpr int kTileBytes = 32768;
-constexpr int kStages = 6;
+template <int ES>
+struct FastCfg;
+// 32-bit elements: 8 scanner warps, 32 KiB tiles (8192 elements), 6 stages
+template <>
+struct FastCfg<4> {
+    static constexpr int kScanWarps = 8, kTileBytes = 32768, kStages = 6;
+};
+// 64-bit elements: 12 scanner warps, 48 KiB tiles (6144 elements), 4 stages
+// (profiles/r1_lab_ws2_wide.json: 398 Gelem/s vs 370 for the 32-bit shape)
+template <>
+struct FastCfg<8> {
+    static constexpr int kScanWarps = 12, kTileBytes = 49152, kStages = 4;
+};
 constexpr int kThreads = 512;  // generic path
+constexpr int kGenTileBytes = 32768;
 constexpr int kGenStages = 2;
 constexpr int kReduceThreads = 512;
 
@@ -49,6 +61,9 @@ struct DebugCfg {
     int64_t spin_budget = 0;
     int64_t corrupt = -1;
     int protocol = 0;
+    int64_t delay_red_ns = 0;
+    int64_t delay_scan_ns = 0;
+    int64_t stall_tile = -1;
     bool armed() const { return spin_budget > 0 || corrupt >= 0 || protocol != 0; }
 };
 std::mutex g_dbg_mu;
@@ -87,14 +102,19 @@ int elem_size(ls_dtype dt) {
     }
 }
 
-int64_t tile_elems(ls_dtype dt) { return kTileBytes / elem_size(dt); }
-int64_t num_tiles(ls_dtype dt, int64_t n) { return (n + tile_elems(dt) - 1) / tile_elems(dt); }
-
-template <typename T>
-size_t ws_smem() { return scan_ws_smem_bytes<T, kScanWarps, kTileBytes, kStages>(); }
+int fast_tile_bytes(int es) { return es == 4 ? FastCfg<4>::kTileBytes : FastCfg<8>::kTileBytes; }
+int64_t tile_elems(ls_dtype dt, bool fast) {
+    return (fast ? fast_tile_bytes(elem_size(dt)) : kGenTileBytes) / elem_size(dt);
+}
+int64_t num_tiles(ls_dtype dt, int64_t n, bool fast) {
+    const int64_t te = tile_elems(dt, fast);
+    return (n + te - 1) / te;
+}
+// the workspace must fit the path with the smaller tiles
+int64_t max_tiles(ls_dtype dt, int64_t n) { return std::max(num_tiles(dt, n, true), num_tiles(dt, n, false)); }
 
 size_t gen_smem(int es) {
-    return (size_t)kGenStages * kTileBytes + (size_t)kGenStages * 8 + (size_t)(2 * (kThreads / 32) + 1) * es + 16;
+    return (size_t)kGenStages * kGenTileBytes + (size_t)kGenStages * 8 + (size_t)(2 * (kThreads / 32) + 1) * es + 16;
 }
 
 // ----------------------------------------------------- kernel dispatch --
@@ -108,12 +128,13 @@ struct Launch {
 
 template <typename T>
 Launch pick_typed(bool excl, bool fast) {
+    using C = FastCfg<sizeof(T)>;
     if (fast)
-        return {excl ? &scan_ws_kernel<T, kScanWarps, kTileBytes, kStages, true>
-                     : &scan_ws_kernel<T, kScanWarps, kTileBytes, kStages, false>,
-                kWsThreads, ws_smem<T>()};
-    return {excl ? &scan_kernel<T, kThreads, kTileBytes, kGenStages, true, false>
-                 : &scan_kernel<T, kThreads, kTileBytes, kGenStages, false, false>,
+        return {excl ? &scan_ws2_kernel<T, C::kScanWarps, C::kTileBytes, C::kStages, true>
+                     : &scan_ws2_kernel<T, C::kScanWarps, C::kTileBytes, C::kStages, false>,
+                (C::kScanWarps + 3) * 32, scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>()};
+    return {excl ? &scan_kernel<T, kThreads, kGenTileBytes, kGenStages, true, false>
+                 : &scan_kernel<T, kThreads, kGenTileBytes, kGenStages, false, false>,
             kThreads, gen_smem(sizeof(T))};
 }
 
@@ -242,7 +263,7 @@ ls_status scan_impl(ls_dtype dt, const void *x, void *y, int64_t n, const void *
     if ((st = device_state(&d)) != LS_OK) return st;
 
     const bool tma = (((uintptr_t)x | (uintptr_t)y) & 15u) == 0;
-    const int64_t M = num_tiles(dt, n);
+    const int64_t M = num_tiles(dt, n, tma);
     const int occ = d->occ[dt][excl][tma];
     const int64_t cap = (int64_t)occ * d->sms;
     const int G = (int)std::min<int64_t>(M, cap);
@@ -260,6 +281,10 @@ ls_status scan_impl(ls_dtype dt, const void *x, void *y, int64_t n, const void *
     p.corrupt_tile = dbg.corrupt;
     p.protocol_checks = dbg.protocol;
     p.experiment = 0;
+    p.delay_red_ns = dbg.delay_red_ns;
+    p.delay_scan_ns = dbg.delay_scan_ns;
+    // a stalled tile without a watchdog would hang the chain forever
+    p.stall_tile = dbg.spin_budget > 0 ? dbg.stall_tile : -1;
 
     // Cooperative launch: the driver refuses a grid that cannot be fully
     // co-resident, which is the deadlock-freedom precondition of the
@@ -314,7 +339,7 @@ int64_t ls_launch_count(void) { return g_launches.load(std::memory_order_relaxed
 
 size_t ls_workspace_bytes(ls_dtype dt, int64_t n) {
     if (!valid_dtype(dt) || n < 0) return 0;
-    const int64_t M = std::max<int64_t>(num_tiles(dt, n), 1);
+    const int64_t M = std::max<int64_t>(max_tiles(dt, n), 1);
     const size_t sw = elem_size(dt) == 4 ? 8 : 16;
     size_t bytes = kSlotBase + 2 * (size_t)M * sw;
     return (bytes + 255) & ~(size_t)255;
@@ -389,6 +414,14 @@ ls_status ls_debug_config(int64_t spin_budget, int64_t corrupt_block, int protoc
     return LS_OK;
 }
 
+ls_status ls_debug_perturb(int64_t reducer_delay_ns, int64_t scanner_delay_ns, int64_t stall_tile) {
+    std::lock_guard<std::mutex> lk(g_dbg_mu);
+    g_dbg.stall_tile = stall_tile >= 0 ? stall_tile : -1;
+    g_dbg.delay_red_ns = reducer_delay_ns > 0 ? reducer_delay_ns : 0;
+    g_dbg.delay_scan_ns = scanner_delay_ns > 0 ? scanner_delay_ns : 0;
+    return LS_OK;
+}
+
 ls_status ls_workspace_error(void *ws, size_t ws_bytes, void *stream) {
     ls_status st = check_ws_header(ws, ws_bytes, kSlotBase);
     if (st != LS_OK) return st;
@@ -401,11 +434,12 @@ ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]) {
     ls_status st = device_state(&d);
     if (st != LS_OK) return st;
     const int occ = d->occ[dt][0][1];
-    const int64_t M = num_tiles(dt, n);
+    const int64_t M = num_tiles(dt, n, true);
+    const Launch L = pick_scan(dt, false, true);
     out[0] = std::min<int64_t>(std::max<int64_t>(M, 1), (int64_t)occ * d->sms);
-    out[1] = kWsThreads;
-    out[2] = tile_elems(dt);
-    out[3] = kStages;
+    out[1] = L.threads;
+    out[2] = tile_elems(dt, true);
+    out[3] = elem_size(dt) == 4 ? FastCfg<4>::kStages : FastCfg<8>::kStages;
     out[4] = occ;
     out[5] = d->sms;
     return LS_OK;

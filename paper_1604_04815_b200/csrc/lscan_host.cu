@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -30,7 +31,15 @@ void set_detail(const std::string &msg);
 namespace {
 
 constexpr int kBufs = 3;
-constexpr size_t kChunkBytes = (size_t)64 << 20;  // 64 MiB per chunk
+constexpr size_t kDefaultChunkMiB = 32;  // per-chunk bytes; LSCAN_HOST_CHUNK_MB overrides
+
+size_t chunk_bytes_from_env() {
+    const char *e = getenv("LSCAN_HOST_CHUNK_MB");
+    long mb = e ? atol(e) : (long)kDefaultChunkMiB;
+    if (mb < 1) mb = 1;
+    if (mb > 1024) mb = 1024;
+    return (size_t)mb << 20;
+}
 
 struct HostCtx {
     bool init = false;
@@ -43,6 +52,7 @@ struct HostCtx {
     void *ws = nullptr;
     size_t ws_bytes = 0;
     cudaEvent_t ev_in[kBufs] = {}, ev_comp[kBufs] = {}, ev_out[kBufs] = {};
+    size_t chunk_bytes = 0;
     std::mutex mu;
 };
 
@@ -67,6 +77,8 @@ ls_status ctx_for(int dev, HostCtx **out) {
     HostCtx *c = g_ctx[dev];
     if (!c->init) {
         c->device = dev;
+        c->chunk_bytes = chunk_bytes_from_env();
+        const size_t kChunkBytes = c->chunk_bytes;
         HC(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking), "stream");
         HC(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking), "stream");
         HC(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking), "stream");
@@ -89,6 +101,7 @@ ls_status ctx_for(int dev, HostCtx **out) {
 }
 
 ls_status ensure_staging(HostCtx *c) {
+    const size_t kChunkBytes = c->chunk_bytes;
     for (int b = 0; b < kBufs; ++b) {
         if (!c->pin_in[b]) HC(cudaHostAlloc(&c->pin_in[b], kChunkBytes, cudaHostAllocDefault), "pinned staging");
         if (!c->pin_out[b]) HC(cudaHostAlloc(&c->pin_out[b], kChunkBytes, cudaHostAllocDefault), "pinned staging");
@@ -132,7 +145,7 @@ extern "C" ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, 
     const bool direct = is_pinned(x) && is_pinned(y);
     if (!direct && (st = ensure_staging(c)) != LS_OK) return st;
 
-    const int64_t chunk = (int64_t)(kChunkBytes / es);
+    const int64_t chunk = (int64_t)(c->chunk_bytes / es);
     const int64_t nchunks = (n + chunk - 1) / chunk;
     const uint8_t *xb = static_cast<const uint8_t *>(x);
     uint8_t *yb = static_cast<uint8_t *>(y);

@@ -97,7 +97,18 @@ struct ScanParams {
     int64_t corrupt_tile;   // -1 = off
     int protocol_checks;
     int experiment;         // lab-only bits: 1 = skip the look-back (timing upper bound, wrong sums)
+    int64_t delay_red_ns;   // debug: reducer sleeps this long on tiles t % 3 == 1 (timing perturbation)
+    int64_t delay_scan_ns;  // debug: scanners sleep this long on tiles t % 3 == 2
+    int64_t stall_tile;     // debug: this tile never publishes its aggregate (needs a spin budget)
 };
+
+__device__ __forceinline__ void debug_sleep(int64_t ns) {
+    while (ns > 0) {
+        const unsigned chunk = ns > 100000 ? 100000u : (unsigned)ns;
+        __nanosleep(chunk);
+        ns -= chunk;
+    }
+}
 
 template <typename T>
 struct Slot {
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const ScanParams p) {
                     S::load(agg, t, w);
                     if (S::decode(w, tag, dummy)) raise_error(hdr, 5u /*LS_ERR_PROTOCOL*/, (uint32_t)t);
                 }
-                S::publish(agg, t, tag, t == p.corrupt_tile ? T(0) : tile_agg);
+                if (t != p.stall_tile || p.spin_budget <= 0) S::publish(agg, t, tag, t == p.corrupt_tile ? T(0) : tile_agg);
             }
             T prefix = T(0);
             const bool has = (p.experiment & 1)

@@ -226,6 +226,7 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws_kernel(const
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+            if (p.delay_red_ns > 0 && t % 3 == 1) debug_sleep(p.delay_red_ns);
             const T a = reduce_stage<T, TILE_BYTES>(stages + s * TILE_BYTES, lane);
             __syncwarp();
             if (lane == 0) {
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws_kernel(const
                     S::load(agg, t, w);
                     if (S::decode(w, tag, dummy)) raise_error(hdr, 5u /*LS_ERR_PROTOCOL*/, (uint32_t)t);
                 }
-                S::publish(agg, t, tag, t == p.corrupt_tile ? T(0) : a);
+                if (t != p.stall_tile || p.spin_budget <= 0) S::publish(agg, t, tag, t == p.corrupt_tile ? T(0) : a);
                 mbar_arrive(&red_done[s]);
             }
         }
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws_kernel(const
             const int64_t t = c + k * G;
             uint8_t *st = stages + s * TILE_BYTES;
             mbar_wait(&full[s], parity);
+            if (p.delay_scan_ns > 0 && t % 3 == 2 && warp == (int)(t % SCAN_WARPS)) debug_sleep(p.delay_scan_ns);
             Regs<T, V> r;
             load_tile_regs<T, V>(st, tid, r);
             T tsum = r.e[0];
@@ -321,6 +323,10 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws_kernel(const
             }
             if (t == M - 1 && tid == SCAN_THREADS - 1 && p.total_out != nullptr)
                 *static_cast<T *>(p.total_out) = acc;
+            // the results overwrite the stage in place: the reducer must be done
+            // reading it (it usually is — it runs ahead — but CTAs whose prefix
+            // does not depend on their own aggregate can get here first)
+            mbar_wait(&red_done[s], parity);
             store_tile_regs<T, V>(st, tid, r);
             fence_proxy_async_smem();
             named_bar_sync(1, SCAN_THREADS);  // (C)

@@ -174,3 +174,36 @@ def check_workspace_error(device: Optional[torch.device] = None) -> None:
     if ws is None:
         return
     raise_for_status(N.lib().ls_workspace_error(ws.data_ptr(), ws.numel(), stream.cuda_stream))
+
+
+class debug:
+    """Context manager arming the device debug hooks (process-wide):
+
+    * ``spin_budget``      look-back watchdog -> ``LivenessError`` (ChainConfig.spin_budget, chained.py:222)
+    * ``corrupt_tile``     that tile publishes the identity (ChainConfig.corrupt_slot, chained.py:224)
+    * ``protocol_checks``  publish-once check -> ``ProtocolViolation`` (chained.py:114-120)
+    * ``reducer_delay_ns`` / ``scanner_delay_ns``  timing perturbation (test_chained.py:239-256)
+    * ``stall_tile``       that tile never publishes (needs ``spin_budget``; test_chained.py:259-272)
+
+    While armed (any of the first three), every scan synchronises and raises
+    the device error word."""
+
+    _lock = threading.Lock()
+
+    def __init__(self, spin_budget: int = 0, corrupt_tile: int = -1, protocol_checks: bool = False,
+                 reducer_delay_ns: int = 0, scanner_delay_ns: int = 0, stall_tile: int = -1):
+        self.args = (spin_budget, corrupt_tile, 1 if protocol_checks else 0)
+        self.perturb = (reducer_delay_ns, scanner_delay_ns, stall_tile)
+
+    def __enter__(self):
+        debug._lock.acquire()
+        L = N.lib()
+        raise_for_status(L.ls_debug_config(*self.args))
+        raise_for_status(L.ls_debug_perturb(*self.perturb))
+        return self
+
+    def __exit__(self, *exc):
+        L = N.lib()
+        L.ls_debug_config(0, -1, 0)
+        L.ls_debug_perturb(0, 0, -1)
+        debug._lock.release()
