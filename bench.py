@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-dtype / CUB side lines")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the sharded (reduce + all-gather + carried scan) path even at world size 1")
     return ap.parse_args()
 
 
@@ -248,7 +250,7 @@ def run_ours(args):
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
-    use_dist = world > 1
+    use_dist = world > 1 or args.force_dist
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     tok = args.dtype
@@ -267,7 +269,7 @@ def run_ours(args):
         from paper_1604_04815_b200.distributed import sharded_scan
 
         def step():
-            sharded_scan(xd, out=None)
+            sharded_scan(xd, out=yd)
     else:
         def step():
             S.inclusive_scan(xd, out=yd)
@@ -347,6 +349,37 @@ def run_ours(args):
         if tok[0] == "i":
             out["e2e"]["validated"] = bool(np.array_equal(yp.numpy()[-1000:], yd.cpu().numpy()[-1000:]))
         del xp, yp
+
+    if not args.no_e2e and use_dist:
+        # each rank: its shard host->device, the sharded scan, device->host
+        from paper_1604_04815_b200.distributed import sharded_scan
+        xp = torch.empty(n, dtype=tdt).pin_memory()
+        yp = torch.empty(n, dtype=tdt).pin_memory()
+        xp.numpy()[:] = xh
+        xe = torch.empty_like(xd)
+
+        def e2e_step():
+            xe.copy_(xp, non_blocking=True)
+            sharded_scan(xe, out=yd)
+            yp.copy_(yd, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        ts = []
+        for _ in range(3):
+            dist.barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            dist.barrier()
+            ts.append(time.perf_counter() - t0)
+        tt = torch.tensor([statistics.median(ts)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+        out["e2e"] = {"value": round(total_elems / e2e_s * 1e-9, 3), "unit": "Gelem/s",
+                      "h2d_bytes_per_step": n * es * world, "d2h_bytes_per_step": n * es * world,
+                      "api": "per rank: pinned shard H2D -> distributed.sharded_scan -> D2H (not overlapped)",
+                      "ms_per_step": round(e2e_s * 1e3, 3)}
+        del xp, yp, xe
 
     # ---- the other dtypes and CUB on the same box (N=1 only)
     if not args.no_sweep and not use_dist:

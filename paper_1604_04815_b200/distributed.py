@@ -44,14 +44,14 @@ class ShardOps:
 
     reduce: Callable[[torch.Tensor], torch.Tensor]                     # shard -> [1] total
     carry: Callable[[torch.Tensor, int], torch.Tensor]                 # (totals[G], rank) -> [1]
-    scan: Callable[[torch.Tensor, Optional[torch.Tensor], bool], torch.Tensor]  # (shard, carry, excl)
+    scan: Callable[..., torch.Tensor]  # (shard, carry, exclusive, out=None) -> scanned shard
 
 
 def cuda_ops() -> ShardOps:
     from . import scan as S
 
-    def _scan(x, carry, exclusive):
-        return (S.exclusive_scan if exclusive else S.inclusive_scan)(x, carry_in=carry)
+    def _scan(x, carry, exclusive, out=None):
+        return (S.exclusive_scan if exclusive else S.inclusive_scan)(x, out, carry_in=carry)
 
     return ShardOps(reduce=S.reduce_sum, carry=S.carry_from_totals, scan=_scan)
 
@@ -73,8 +73,9 @@ def sharded_scan(shard: torch.Tensor, *, exclusive: bool = False, group=None,
         parts = list(totals.split(1))
         dist.all_gather(parts, total, group=group)
     carry = ops.carry(totals, rank) if rank > 0 else None
-    res = ops.scan(shard, carry, exclusive)
-    if out is not None:
+    if out is None:
+        return ops.scan(shard, carry, exclusive)
+    res = ops.scan(shard, carry, exclusive, out=out)
+    if res is not out:
         out.copy_(res)
-        return out
-    return res
+    return out
