@@ -93,12 +93,33 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
                     tma_load_1d(stages + s * TILE_BYTES, x + t0, TILE_BYTES, &full[s], pol);
                 }
             } else {
-                // partial_tail (chained.py:188-202): identity-padded last tile
+                // partial_tail (chained.py:188-202): the 16-byte-aligned prefix of
+                // the last tile by TMA, the ragged vector by plain loads, the rest
+                // of the stage identity-filled with 128-bit shared stores
                 const int64_t valid = p.n - t0;
-                T *sv = reinterpret_cast<T *>(stages + s * TILE_BYTES);
-                for (int i = lane; i < TILE_ELEMS; i += 32) sv[i] = (i < valid) ? x[t0 + i] : T(0);
+                const uint32_t bulk = (uint32_t)((valid * (int64_t)sizeof(T)) & ~(int64_t)15);
+                const int vfirst = (int)(bulk / 16);  // first vector not covered by TMA
+                uint8_t *sb = stages + s * TILE_BYTES;
+                const uint32_t sbase = smem_u32(sb);
+                for (int v = vfirst + 1 + lane; v < TILE_BYTES / 16; v += 32) sts128(sbase + (uint32_t)v * 16u, make_uint4(0, 0, 0, 0));
+                if (lane == 0 && vfirst < TILE_BYTES / 16) {
+                    Regs<T, 1> rv;
+#pragma unroll
+                    for (int e = 0; e < PER; ++e) {
+                        const int64_t i = (int64_t)vfirst * PER + e;
+                        rv.e[e] = i < valid ? x[t0 + i] : T(0);
+                    }
+                    sts128(sbase + (uint32_t)vfirst * 16u, rv.q[0]);
+                }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&full[s]);
+                if (lane == 0) {
+                    if (bulk) {
+                        mbar_arrive_expect_tx(&full[s], bulk);
+                        tma_load_1d(sb, x + t0, bulk, &full[s], pol);
+                    } else {
+                        mbar_arrive(&full[s]);
+                    }
+                }
             }
         };
         for (int64_t k = 0; k < STAGES && k < my_tiles; ++k) load_tile(k);
@@ -239,9 +260,9 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
                     }
                 }
                 const int64_t vec = (int64_t)warp * (WARP_BYTES / 16) + j * 32 + lane;  // 16-byte vector index
-                if (!partial) {
+                if (!partial || (vec + 1) * PER <= valid) {
                     stg128(reinterpret_cast<uint8_t *>(yt) + vec * 16, r.q[j]);
-                } else {
+                } else if (vec * PER < valid) {
 #pragma unroll
                     for (int e = 0; e < PER; ++e)
                         if (vec * PER + e < valid) yt[vec * PER + e] = r.e[j * PER + e];
