@@ -44,6 +44,11 @@ typedef enum {
 
 typedef enum { LS_I32 = 0, LS_I64 = 1, LS_F32 = 2, LS_F64 = 3 } ls_dtype;
 
+/* Scan operators (make_operator, operators.py:111-127): add (identity 0,
+ * integers wrap), max (identity = lowest value / -inf), min (highest / +inf).
+ * Float max/min propagate NaN like numpy.maximum / numpy.minimum. */
+typedef enum { LS_OP_ADD = 0, LS_OP_MAX = 1, LS_OP_MIN = 2 } ls_op;
+
 /* ---- workspace ------------------------------------------------------------
  * The carry-chain buffer (the reference's CommSlots, chained.py:85-150): one
  * write-once slot per data tile plus one per round, epoch-tagged so a call
@@ -55,11 +60,20 @@ ls_status ls_workspace_init(void *ws, size_t ws_bytes, void *stream);
 
 /* ---- device scans (the hot path) -------------------------------------------
  * y[j] = carry (+) x[0] (+) ... (+) x[j]            (inclusive)
- * y[j] = carry (+) x[0] (+) ... (+) x[j-1]          (exclusive; y[0] = carry)
+ * y[j] = carry (+) x[0] (+) ... (+) x[j-1]          (exclusive; y[0] = carry,
+ *                                                    or the identity)
  * carry_in: nullable device scalar (identity when NULL) — the multi-GPU
  *   carry from lower shards.
- * total_out: nullable device scalar receiving carry (+) sum(x).
- * Replaces chained_scan (chained.py:316) for op "add". */
+ * total_out: nullable device scalar receiving carry (+) x[0] (+) ... (+) x[n-1];
+ *   must not alias carry_in.
+ * Replaces chained_scan (chained.py:316) for the given operator. */
+ls_status ls_inclusive_scan(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
+                            const void *carry_in, void *total_out,
+                            void *ws, size_t ws_bytes, void *stream);
+ls_status ls_exclusive_scan(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
+                            const void *carry_in, void *total_out,
+                            void *ws, size_t ws_bytes, void *stream);
+/* The north-star sum scans: ls_*_scan with LS_OP_ADD. */
 ls_status ls_inclusive_sum(ls_dtype dt, const void *x, void *y, int64_t n,
                            const void *carry_in, void *total_out,
                            void *ws, size_t ws_bytes, void *stream);
@@ -67,15 +81,19 @@ ls_status ls_exclusive_sum(ls_dtype dt, const void *x, void *y, int64_t n,
                            const void *carry_in, void *total_out,
                            void *ws, size_t ws_bytes, void *stream);
 
-/* total_out = sum(x) (device scalar), deterministic for a given device; the
- * per-shard total of the multi-GPU carry exchange. */
+/* total_out = x[0] (+) ... (+) x[n-1] (device scalar; identity for n == 0),
+ * deterministic for a given device; the per-shard total of the multi-GPU
+ * carry exchange. */
+ls_status ls_reduce(ls_op op, ls_dtype dt, const void *x, int64_t n, void *total_out,
+                    void *ws, size_t ws_bytes, void *stream);
 ls_status ls_reduce_sum(ls_dtype dt, const void *x, int64_t n, void *total_out,
                         void *ws, size_t ws_bytes, void *stream);
 
-/* carry_out[g] = t[0] (+) ... (+) t[g-1] for g < count (exclusive scan of
- * the gathered per-rank totals, fixed left-to-right order).
- * t and carry_out are device arrays of `count` scalars. */
-ls_status ls_carry_from_totals(ls_dtype dt, const void *totals, int64_t count,
+/* carry_out = t[0] (+) ... (+) t[rank-1] (identity for rank 0): the fold of
+ * the gathered per-rank totals in fixed left-to-right order (SURVEY §8e
+ * step 3).  totals is a device array of `count` scalars, carry_out a device
+ * scalar. */
+ls_status ls_carry_from_totals(ls_op op, ls_dtype dt, const void *totals, int64_t count,
                                int64_t rank, void *carry_out, void *stream);
 
 /* ---- host-buffer entry (what chained_scan(problem) does with numpy arrays) --
@@ -83,6 +101,8 @@ ls_status ls_carry_from_totals(ls_dtype dt, const void *totals, int64_t count,
  * is streamed through the device in chunks with copy-in, scan and copy-out
  * overlapped on three streams, the carry chained on the device between
  * chunks.  Blocks until y is complete.  device < 0 = current device. */
+ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
+                       int exclusive, int device);
 ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n,
                                 int exclusive, int device);
 

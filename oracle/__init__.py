@@ -86,28 +86,41 @@ def generate_input_chunks(n: int, tok, seed, chunk: int) -> Iterator[np.ndarray]
         done += k
 
 
-def sequential_scan(x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+# operators.py:111-127: ufunc and identity per operator
+UFUNCS = {"add": np.add, "max": np.maximum, "min": np.minimum}
+
+
+def identity(op: str, dtype) -> object:
+    dtype = np.dtype(dtype)
+    if op == "add":
+        return dtype.type(0)
+    if op == "max":
+        return dtype.type(np.iinfo(dtype).min if dtype.kind == "i" else -np.inf)
+    return dtype.type(np.iinfo(dtype).max if dtype.kind == "i" else np.inf)
+
+
+def sequential_scan(x: np.ndarray, out: Optional[np.ndarray] = None, op: str = "add") -> np.ndarray:
     """The oracle (reference.py:61-67 / operators.py:87-94): strict left fold
-    in the element dtype; integer overflow wraps (two's complement)."""
+    of ``op`` in the element dtype; integer overflow wraps (two's complement)."""
     x = np.asarray(x)
     if out is None:
         out = np.empty_like(x)
     if x.size == 0:
         return out
     with np.errstate(over="ignore"):
-        np.add.accumulate(x, out=out, dtype=x.dtype)
+        UFUNCS[op].accumulate(x, out=out, dtype=x.dtype)
     return out
 
 
-def exclusive_scan(x: np.ndarray) -> np.ndarray:
-    """Derived exclusive scan: y[0] = 0, y[j] = inclusive[j-1]."""
+def exclusive_scan(x: np.ndarray, op: str = "add") -> np.ndarray:
+    """Derived exclusive scan: y[0] = identity, y[j] = inclusive[j-1]."""
     x = np.asarray(x)
     out = np.empty_like(x)
     if x.size == 0:
         return out
-    out[0] = 0
+    out[0] = identity(op, x.dtype)
     if x.size > 1:
-        sequential_scan(x[:-1], out=out[1:])
+        sequential_scan(x[:-1], out=out[1:], op=op)
     return out
 
 
@@ -117,19 +130,19 @@ def float_add_envelope(x: np.ndarray, eps_rel: float) -> np.ndarray:
 
 
 def validate_output(x: np.ndarray, y: np.ndarray, ref: Optional[np.ndarray] = None,
-                    exclusive: bool = False) -> Optional[str]:
+                    exclusive: bool = False, op: str = "add") -> Optional[str]:
     """bench.py:95-114: None if y matches the oracle, else a message.
 
-    Integers must be bit-exact; float add must lie within
+    Integers and max/min must be bit-exact; float add must lie within
     ``FLOAT_EPS_REL * cumsum|x|`` (f32 1e-5, f64 1e-12).  For the exclusive
     mode the envelope is the inclusive one shifted by one element."""
     x = np.asarray(x)
     y = np.asarray(y)
     if ref is None:
-        ref = exclusive_scan(x) if exclusive else sequential_scan(x)
+        ref = exclusive_scan(x, op) if exclusive else sequential_scan(x, op=op)
     if y.shape != ref.shape:
         return f"shape mismatch {y.shape} vs {ref.shape}"
-    if x.dtype.kind == "i":
+    if x.dtype.kind == "i" or op in ("max", "min"):
         if np.array_equal(ref, y):
             return None
         bad = np.nonzero(ref != y)[0]

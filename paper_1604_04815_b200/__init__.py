@@ -39,7 +39,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-level API loaded lazily so the numpy surface imports without torch
-    if name in ("inclusive_scan", "exclusive_scan", "reduce_sum", "carry_from_totals", "query_config"):
+    if name in ("inclusive_scan", "exclusive_scan", "reduce", "reduce_sum", "carry_from_totals", "query_config"):
         from . import scan
         return getattr(scan, name)
     raise AttributeError(name)
@@ -50,5 +50,5 @@ __all__ = [
     "ProtocolViolation", "ScanOperator", "ScanProblem", "ShapeError", "SpinPolicy",
     "UnsupportedOperatorError", "WorkspaceError", "chained_exclusive_scan", "chained_scan",
     "default_worker_count", "dtype_token", "make_operator", "parse_dtype", "run_algorithm",
-    "inclusive_scan", "exclusive_scan", "reduce_sum", "carry_from_totals", "query_config",
+    "inclusive_scan", "exclusive_scan", "reduce", "reduce_sum", "carry_from_totals", "query_config",
 ]

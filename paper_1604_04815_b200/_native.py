@@ -20,8 +20,10 @@ INCLUDE = os.path.join(REPO_DIR, "include")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
 
-SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_lab.cu"]
-HEADERS = ["lscan_kernels.cuh", "lscan_ptx.cuh", "lscan_scan_ws.cuh", "lscan_scan_ws2.cuh"]
+SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_lab.cu", "lscan_inst_i32.cu", "lscan_inst_i64.cu",
+           "lscan_inst_f32.cu", "lscan_inst_f64.cu"]
+HEADERS = ["lscan_common.cuh", "lscan_ptx.cuh", "lscan_generic.cuh", "lscan_scan_ws2.cuh", "lscan_dispatch.h",
+           "lscan_inst.cuh"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 # ls_status (include/lscan.h)
@@ -36,9 +38,14 @@ LS_ERR_WORKSPACE = 6
 # ls_dtype
 LS_I32, LS_I64, LS_F32, LS_F64 = 0, 1, 2, 3
 
+# ls_op
+LS_OP_ADD, LS_OP_MAX, LS_OP_MIN = 0, 1, 2
+OPS = {"add": LS_OP_ADD, "max": LS_OP_MAX, "min": LS_OP_MIN}
+
 EXPORTED = [
-    "ls_workspace_bytes", "ls_workspace_init", "ls_inclusive_sum", "ls_exclusive_sum",
-    "ls_reduce_sum", "ls_carry_from_totals", "ls_inclusive_sum_host", "ls_debug_config", "ls_debug_perturb",
+    "ls_workspace_bytes", "ls_workspace_init", "ls_inclusive_scan", "ls_exclusive_scan", "ls_inclusive_sum",
+    "ls_exclusive_sum", "ls_reduce", "ls_reduce_sum", "ls_carry_from_totals", "ls_scan_host",
+    "ls_inclusive_sum_host", "ls_debug_config", "ls_debug_perturb",
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
     "ls_query_config", "ls_launch_count",
 ]
@@ -57,19 +64,30 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, extra: Optional[List[str]] = None) -> str:
-    """nvcc the CUDA sources into ``_lib/liblscan.so`` for sm_100a."""
+    """nvcc the CUDA sources into ``_lib/liblscan.so`` for sm_100a (one
+    object per translation unit, compiled in parallel, then linked)."""
     if not force and not needs_build():
         return LIB_PATH
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(LIB_DIR, exist_ok=True)
+    objdir = os.path.join(LIB_DIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, "-O3", "-std=c++17", *ARCH_FLAGS, "-lineinfo", "-Xcompiler", "-fPIC",
-           "-shared", f"-I{INCLUDE}", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+    flags = ["-O3", "-std=c++17", *ARCH_FLAGS, "-lineinfo", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+        flags.append("-Xptxas=-v")
     if extra:
-        cmd[1:1] = extra
-    subprocess.run(cmd, check=True)
+        flags += extra
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        subprocess.run([nvcc, *flags, "-c", "-o", obj, os.path.join(CSRC, src)], check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    tmp = LIB_PATH + ".tmp"
+    subprocess.run([nvcc, *ARCH_FLAGS, "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -95,10 +113,14 @@ def lib():
         sig = {
             "ls_workspace_bytes": (sz, [ci, i64]),
             "ls_workspace_init": (ci, [vp, sz, vp]),
+            "ls_inclusive_scan": (ci, [ci, ci, vp, vp, i64, vp, vp, vp, sz, vp]),
+            "ls_exclusive_scan": (ci, [ci, ci, vp, vp, i64, vp, vp, vp, sz, vp]),
             "ls_inclusive_sum": (ci, [ci, vp, vp, i64, vp, vp, vp, sz, vp]),
             "ls_exclusive_sum": (ci, [ci, vp, vp, i64, vp, vp, vp, sz, vp]),
+            "ls_reduce": (ci, [ci, ci, vp, i64, vp, vp, sz, vp]),
             "ls_reduce_sum": (ci, [ci, vp, i64, vp, vp, sz, vp]),
-            "ls_carry_from_totals": (ci, [ci, vp, i64, i64, vp, vp]),
+            "ls_carry_from_totals": (ci, [ci, ci, vp, i64, i64, vp, vp]),
+            "ls_scan_host": (ci, [ci, ci, vp, vp, i64, ci, ci]),
             "ls_inclusive_sum_host": (ci, [ci, vp, vp, i64, ci, ci]),
             "ls_debug_config": (ci, [i64, i64, ci]),
             "ls_debug_perturb": (ci, [i64, i64, i64]),

@@ -4,13 +4,14 @@
 signature and contract of chainscan's ``chained_scan`` (chained.py:316-357):
 
 * ``problem`` is a ``ScanProblem`` (this package's or the reference's own —
-  only ``x``, ``op`` and ``out`` are read); ``op.name`` must be ``"add"``;
+  only ``x``, ``op`` and ``out`` are read); ``op.name`` is ``"add"``,
+  ``"max"`` or ``"min"`` (operators.py:111-127);
 * the result lands in ``problem.out`` when given (it may alias ``x``, an
   in-place scan) or in a fresh array, and that array object is returned;
 * ``n == 0`` returns the (empty) output untouched;
 * integers wrap (two's complement) and are bit-identical to the sequential
-  oracle; floats match it within the reference envelope
-  ``1e-5 / 1e-12 * cumsum|x|`` (bench.py:49, :90-114).
+  oracle, as are max/min for every dtype; float add matches it within the
+  reference envelope ``1e-5 / 1e-12 * cumsum|x|`` (bench.py:49, :90-114).
 
 The scan runs on the device through the C ABI (``ls_inclusive_sum_host``):
 the host array is streamed through the GPU in chunks with copy-in, scan and
@@ -90,7 +91,8 @@ class ChainConfig:
                              f"choose from {BLOCK_SCAN_MODES}")
 
 
-def _device_debug_scan(x: np.ndarray, out: np.ndarray, config: ChainConfig, exclusive: bool) -> None:
+def _device_debug_scan(x: np.ndarray, out: np.ndarray, config: ChainConfig, exclusive: bool,
+                       op_name: str) -> None:
     """One device launch over the whole array with the debug hooks armed
     (so that ``corrupt_slot`` names a tile of this array, not of a chunk)."""
     import torch
@@ -99,7 +101,7 @@ def _device_debug_scan(x: np.ndarray, out: np.ndarray, config: ChainConfig, excl
     with S.debug(spin_budget=int(config.spin_budget or 0),
                  corrupt_tile=-1 if config.corrupt_slot is None else int(config.corrupt_slot)):
         xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
-        yd = S.exclusive_scan(xd) if exclusive else S.inclusive_scan(xd)
+        yd = (S.exclusive_scan if exclusive else S.inclusive_scan)(xd, op=op_name)
         out[...] = yd.cpu().numpy()
 
 
@@ -126,24 +128,25 @@ def _scan_host(problem, config: Optional[ChainConfig], exclusive: bool) -> np.nd
     if not x.flags.c_contiguous:
         x = np.ascontiguousarray(x)
     if config is not None and (config.spin_budget or config.corrupt_slot is not None):
-        _device_debug_scan(x, out, config, exclusive)
+        _device_debug_scan(x, out, config, exclusive, op.name)
         return out
     aliased = problem.out is not None and np.shares_memory(out, x)
     if aliased and out.ctypes.data != x.ctypes.data:
         raise ShapeError("out overlaps x without being the same array (only exact in-place is supported)")
-    rc = N.lib().ls_inclusive_sum_host(NP_DT[dtype], x.ctypes.data, out.ctypes.data, n,
-                                       1 if exclusive else 0, -1)
+    rc = N.lib().ls_scan_host(N.OPS[op.name], NP_DT[dtype], x.ctypes.data, out.ctypes.data, n,
+                              1 if exclusive else 0, -1)
     raise_for_status(rc)
     return out
 
 
 def chained_scan(problem: ScanProblem, config: Optional[ChainConfig] = None) -> np.ndarray:
-    """Inclusive sum-scan of ``problem.x`` on the GPU (chained.py:316-357)."""
+    """Inclusive scan of ``problem.x`` under ``problem.op`` (add / max / min)
+    on the GPU (chained.py:316-357)."""
     return _scan_host(problem, config, exclusive=False)
 
 
 def chained_exclusive_scan(problem: ScanProblem, config: Optional[ChainConfig] = None) -> np.ndarray:
-    """Exclusive variant (derived mode): y[0] = 0, y[j] = x[0] + ... + x[j-1]."""
+    """Exclusive variant (derived mode): y[0] = identity, y[j] = x[0] (+) ... (+) x[j-1]."""
     return _scan_host(problem, config, exclusive=True)
 
 

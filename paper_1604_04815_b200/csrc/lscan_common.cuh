@@ -1,0 +1,275 @@
+// lscan_common.cuh — pieces shared by every scan kernel: element types and
+// scan operators, the workspace layout, the epoch-tagged carry-chain slots,
+// register-tile helpers and warp-level scans.
+//
+// Operators mirror chainscan/operators.py:111-127: add (identity 0; integers
+// wrap modulo 2^width, operators.py:74-100), max (identity = lowest value,
+// -inf for floats) and min (highest, +inf).  apply(a, b) takes the
+// lower-index operand first (operators.py:13-15).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+#include "lscan_ptx.cuh"
+
+namespace lscan {
+
+// ------------------------------------------------------------------------------
+// element bit casts (the slot protocol moves raw bits)
+template <typename T>
+struct Elem;
+template <>
+struct Elem<int32_t> {
+    using Bits = uint32_t;
+    __device__ static Bits bits(int32_t v) { return (uint32_t)v; }
+    __device__ static int32_t from(Bits b) { return (int32_t)b; }
+};
+template <>
+struct Elem<float> {
+    using Bits = uint32_t;
+    __device__ static Bits bits(float v) { return __float_as_uint(v); }
+    __device__ static float from(Bits b) { return __uint_as_float(b); }
+};
+template <>
+struct Elem<int64_t> {
+    using Bits = uint64_t;
+    __device__ static Bits bits(int64_t v) { return (uint64_t)v; }
+    __device__ static int64_t from(Bits b) { return (int64_t)b; }
+};
+template <>
+struct Elem<double> {
+    using Bits = uint64_t;
+    __device__ static Bits bits(double v) { return (uint64_t)__double_as_longlong(v); }
+    __device__ static double from(Bits b) { return __longlong_as_double((long long)b); }
+};
+
+// ------------------------------------------------------------------------------
+// scan operators (ls_op in include/lscan.h: 0 add, 1 max, 2 min)
+struct OpAdd {
+    static constexpr int code = 0;
+    template <typename T>
+    __device__ __forceinline__ static T apply(T a, T b) {
+        if constexpr (std::is_integral<T>::value) {
+            using U = typename std::make_unsigned<T>::type;
+            return (T)((U)a + (U)b);  // two's-complement wrap, no UB
+        } else {
+            return a + b;
+        }
+    }
+    template <typename T>
+    __device__ __forceinline__ static T identity() { return T(0); }
+};
+
+struct OpMax {
+    static constexpr int code = 1;
+    template <typename T>
+    __device__ __forceinline__ static T apply(T a, T b) {
+        if constexpr (std::is_integral<T>::value) {
+            return a > b ? a : b;
+        } else {
+            // numpy.maximum: a NaN operand propagates
+            return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+        }
+    }
+    template <typename T>
+    __device__ __forceinline__ static T identity() {
+        if constexpr (std::is_same<T, int32_t>::value) return (int32_t)0x80000000u;
+        else if constexpr (std::is_same<T, int64_t>::value) return (int64_t)0x8000000000000000ull;
+        else return -(T)INFINITY;
+    }
+};
+
+struct OpMin {
+    static constexpr int code = 2;
+    template <typename T>
+    __device__ __forceinline__ static T apply(T a, T b) {
+        if constexpr (std::is_integral<T>::value) {
+            return a < b ? a : b;
+        } else {
+            return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+        }
+    }
+    template <typename T>
+    __device__ __forceinline__ static T identity() {
+        if constexpr (std::is_same<T, int32_t>::value) return (int32_t)0x7fffffff;
+        else if constexpr (std::is_same<T, int64_t>::value) return (int64_t)0x7fffffffffffffffll;
+        else return (T)INFINITY;
+    }
+};
+
+// ------------------------------------------------------------------------------
+// workspace layout (bytes):
+//   [0, 128)                               Header
+//   [128, 128 + kMaxGrid*8)                reduce partials (raw values, untagged)
+//   [kSlotBase, kSlotBase + M*SW)          tile aggregate slots A[t]
+//   [.., + M*SW)                           round prefix slots R[r]   (rounds <= M)
+// SW = 8 (32-bit T) or 16 (64-bit T).  Partials live apart from the tagged
+// slots so a raw value can never be mistaken for an epoch tag.
+struct Header {
+    uint32_t epoch;       // last completed call's tag (0 after init)
+    uint32_t done;        // CTAs finished in the current call
+    uint32_t error;       // first ls_status error code raised on the device
+    uint32_t error_tile;  // tile (or slot) index of that error
+    uint32_t pad[28];
+};
+static_assert(sizeof(Header) == 128, "header is one 128-byte line");
+
+constexpr int kMaxGrid = 4096;
+constexpr size_t kSlotBase = sizeof(Header) + (size_t)kMaxGrid * 8;
+
+struct ScanParams {
+    const void *x;
+    void *y;
+    int64_t n;
+    const void *carry_in;   // device scalar or nullptr
+    void *total_out;        // device scalar or nullptr
+    uint8_t *ws;
+    int64_t num_tiles;      // M
+    int64_t spin_budget;    // 0 = unlimited
+    int64_t corrupt_tile;   // -1 = off
+    int protocol_checks;
+    int experiment;         // lab-only bits: 1 = skip the look-back (timing upper bound, wrong sums)
+    int64_t delay_red_ns;   // debug: reducer sleeps this long on tiles t % 3 == 1 (timing perturbation)
+    int64_t delay_scan_ns;  // debug: scanners sleep this long on tiles t % 3 == 2
+    int64_t stall_tile;     // debug: this tile never publishes its aggregate (needs a spin budget)
+};
+
+__device__ __forceinline__ void debug_sleep(int64_t ns) {
+    while (ns > 0) {
+        const unsigned chunk = ns > 100000 ? 100000u : (unsigned)ns;
+        __nanosleep(chunk);
+        ns -= chunk;
+    }
+}
+
+// One write-once carry-chain slot per tile / round.  Each 64-bit word holds
+// (epoch tag : 32 | 32 value bits); 64-bit values use two words.  A reader
+// accepts the slot only when every word carries the current call's tag, so
+// the single-copy atomicity of a 64-bit access is the whole handshake.
+template <typename T>
+struct Slot {
+    static constexpr int W = sizeof(T) / 4;  // 64-bit words per slot
+    __device__ static void publish(uint64_t *arr, int64_t idx, uint32_t tag, T v) {
+        uint64_t *p = arr + idx * W;
+        const uint64_t b = (uint64_t)Elem<T>::bits(v);
+        slot_st(p, ((uint64_t)tag << 32) | (b & 0xffffffffull));
+        if constexpr (W == 2) slot_st(p + 1, ((uint64_t)tag << 32) | (b >> 32));
+    }
+    __device__ static bool decode(const uint64_t (&w)[W], uint32_t tag, T &v) {
+        if constexpr (W == 1) {
+            v = Elem<T>::from((uint32_t)w[0]);
+            return (uint32_t)(w[0] >> 32) == tag;
+        } else {
+            v = Elem<T>::from((w[0] & 0xffffffffull) | (w[1] << 32));
+            return (uint32_t)(w[0] >> 32) == tag && (uint32_t)(w[1] >> 32) == tag;
+        }
+    }
+    __device__ static void load(const uint64_t *arr, int64_t idx, uint64_t (&w)[W]) {
+        const uint64_t *p = arr + idx * W;
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[i] = slot_ld(p + i);
+    }
+};
+
+__device__ __forceinline__ void raise_error(Header *h, uint32_t code, uint32_t where) {
+    if (atomicCAS(&h->error, 0u, code) == 0u) h->error_tile = where;
+}
+
+// The last CTA to finish records this call's tag as the workspace epoch.
+__device__ __forceinline__ void epoch_handover(Header *hdr, uint32_t tag, int grid) {
+    const uint32_t old = atom_add_acqrel_u32(&hdr->done, 1u);
+    if (old == (uint32_t)grid - 1u) {
+        st_relaxed_u32(&hdr->done, 0u);
+        st_relaxed_u32(&hdr->epoch, tag);
+    }
+}
+
+__device__ __forceinline__ uint32_t call_tag(Header *hdr) {
+    const uint32_t prev = ld_relaxed_u32(&hdr->epoch);
+    return (prev + 1u) == 0u ? 1u : prev + 1u;
+}
+
+// ------------------------------------------------------------------------------
+template <typename T, int V>
+union Regs {
+    uint4 q[V];
+    T e[V * 16 / sizeof(T)];
+};
+
+// 16 bytes of identity elements
+template <typename T, typename OP>
+__device__ __forceinline__ uint4 identity_vec() {
+    Regs<T, 1> r;
+#pragma unroll
+    for (int e = 0; e < 16 / (int)sizeof(T); ++e) r.e[e] = OP::template identity<T>();
+    return r.q[0];
+}
+
+// barrel rotation of a thread's 16-byte vectors (bank-conflict-free LDS/STS
+// of a thread-contiguous tile): a'[i] = a[(i + r) mod V]
+template <int V>
+__device__ __forceinline__ void rotate_left(uint4 (&a)[V], int r) {
+#pragma unroll
+    for (int b = 1; b < V; b <<= 1) {
+        const bool take = (r & b) != 0;
+        uint4 t[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) t[i] = a[(i + b) % V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            a[i].x = take ? t[i].x : a[i].x;
+            a[i].y = take ? t[i].y : a[i].y;
+            a[i].z = take ? t[i].z : a[i].z;
+            a[i].w = take ? t[i].w : a[i].w;
+        }
+    }
+}
+
+// rotation that spreads the 8 threads of one LDS.128 phase over all 32 banks
+template <int V>
+__device__ __forceinline__ int vec_rot(int tid) {
+    if constexpr (V >= 8) return tid & 7;
+    else if constexpr (V == 1) return 0;
+    else return (tid / (8 / V)) & (V - 1);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void load_tile_regs(const uint8_t *stage, int tid, Regs<T, V> &r) {
+    const int rot = vec_rot<V>(tid);
+    const uint32_t base = smem_u32(stage) + (uint32_t)tid * (V * 16);
+#pragma unroll
+    for (int u = 0; u < V; ++u) r.q[u] = lds128(base + (uint32_t)(((u + rot) & (V - 1)) * 16));
+    rotate_left<V>(r.q, (V - rot) & (V - 1));  // r.q[j] now holds vector j
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void store_tile_regs(uint8_t *stage, int tid, Regs<T, V> &r) {
+    const int rot = vec_rot<V>(tid);
+    const uint32_t base = smem_u32(stage) + (uint32_t)tid * (V * 16);
+    rotate_left<V>(r.q, rot);  // r.q[u] now holds vector (u + rot) mod V
+#pragma unroll
+    for (int u = 0; u < V; ++u) sts128(base + (uint32_t)(((u + rot) & (V - 1)) * 16), r.q[u]);
+}
+
+// Hillis-Steele over the 32 lanes (warp.py:93-109), lower-index operand first
+template <typename T, typename OP>
+__device__ __forceinline__ T warp_inclusive_scan(T v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const T o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v = OP::apply(o, v);
+    }
+    return v;
+}
+
+// fixed xor-butterfly: every lane ends with bit-identical results because
+// each level combines a commutative pair
+template <typename T, typename OP>
+__device__ __forceinline__ T warp_reduce_fixed(T v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v = OP::apply(v, __shfl_xor_sync(0xffffffffu, v, d));
+    return v;
+}
+
+}  // namespace lscan

@@ -1,0 +1,51 @@
+// lscan_dispatch.h — internal: per-dtype kernel tables built in the
+// lscan_inst_*.cu translation units (compiled in parallel) and consumed by
+// lscan_api.cu.  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lscan_common.cuh"
+
+namespace lscan {
+
+// ---- geometry (chosen from the lab sweeps) --------------
+template <int ES>
+struct FastCfg;
+// 32-bit elements: 8 scanner warps, 32 KiB tiles (8192 elements), 6 stages
+template <>
+struct FastCfg<4> {
+    static constexpr int kScanWarps = 8, kTileBytes = 32768, kStages = 6;
+};
+// 64-bit elements: 12 scanner warps, 48 KiB tiles (6144 elements), 4 stages
+template <>
+struct FastCfg<8> {
+    static constexpr int kScanWarps = 12, kTileBytes = 49152, kStages = 4;
+};
+constexpr int kGenThreads = 512;  // generic (unaligned) path
+constexpr int kGenTileBytes = 32768;
+constexpr int kReduceThreads = 512;
+constexpr int kNumOps = 3;  // ls_op: add, max, min
+
+struct Launch {
+    void (*fn)(const ScanParams);
+    int threads;
+    size_t smem;
+    int tile_bytes;
+    int stages;
+};
+
+struct DtypeKernels {
+    Launch scan[kNumOps][2][2];  // [op][exclusive][fast]
+    const void *reduce_fn[kNumOps];
+    void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s);
+    void (*launch_carry)(int op, const void *totals, int64_t rank, void *carry_out, cudaStream_t s);
+};
+
+const DtypeKernels &kernels_i32();
+const DtypeKernels &kernels_i64();
+const DtypeKernels &kernels_f32();
+const DtypeKernels &kernels_f64();
+
+}  // namespace lscan

@@ -1,0 +1,288 @@
+// lscan_generic.cuh — the sequential persistent scan for arbitrary element
+// alignment (pointers that are not 16-byte aligned cannot use TMA or 128-bit
+// global accesses).
+//
+// One CTA runs the reference worker's per-block sequence in order
+// (chainscan/chained.py:237-249): coalesced element loads of the tile into
+// shared memory (identity-padded, partial_tail chained.py:188-202), a
+// conflict-free register tile (rotated 128-bit shared loads), thread-serial +
+// warp-shuffle + shared-memory block scan (Alg. 2/3), publish A[t], round
+// look-back (the same slot protocol as the hot kernel), carry-seeded fold
+// (Alg. 5), coalesced element stores.  The look-back sits on the critical
+// path here, which is why the aligned hot path is warp-specialised
+// (lscan_scan_ws2.cuh).
+#pragma once
+#include "lscan_common.cuh"
+
+namespace lscan {
+
+// Round look-back executed by one warp: prefix of tile t = r*G + c is
+// R[r-1] (+) A[rG] (+) ... (+) A[rG+c-1], summed in a fixed order.
+template <typename T, typename OP>
+__device__ __forceinline__ bool round_lookback(const uint64_t *agg, const uint64_t *rnd, int64_t r, int c, int G,
+                                               uint32_t tag, const T *carry_in, int lane, int64_t spin_budget,
+                                               Header *hdr, T &prefix) {
+    using S = Slot<T>;
+    constexpr int U = 4;  // slots in flight per lane per pass
+    T acc = OP::template identity<T>();
+    int64_t probes = 0;
+    bool dead = false;
+    const int64_t base_t = r * (int64_t)G;
+    for (int base = 0; base < c && !dead; base += 32 * U) {
+        uint64_t w[U][S::W];
+        bool need[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * 32 + lane;
+            need[u] = j < c;
+            if (need[u]) S::load(agg, base_t + j, w[u]);
+        }
+        T val[U];
+        while (true) {
+            bool ok = true;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (need[u]) {
+                    if (S::decode(w[u], tag, val[u])) need[u] = false;
+                    else ok = false;
+                }
+            }
+            if (__all_sync(0xffffffffu, ok)) break;
+            if (spin_budget > 0 && ++probes > spin_budget) {
+                if (lane == 0) raise_error(hdr, 4u /*LS_ERR_LIVENESS*/, (uint32_t)(base_t + c));
+                dead = true;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (need[u]) { val[u] = OP::template identity<T>(); need[u] = false; }
+                break;
+            }
+            __nanosleep(64);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = base + u * 32 + lane;
+                if (need[u]) S::load(agg, base_t + j, w[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * 32 + lane;
+            if (j < c) acc = OP::apply(acc, val[u]);  // lane-serial, ascending j
+        }
+    }
+    const T asum = warp_reduce_fixed<T, OP>(acc);
+    bool has = false;
+    T rp = OP::template identity<T>();
+    if (r > 0) {
+        uint64_t w[S::W];
+        S::load(rnd, r - 1, w);
+        while (!S::decode(w, tag, rp)) {
+            if (spin_budget > 0 && ++probes > spin_budget) {
+                if (lane == 0) raise_error(hdr, 4u, (uint32_t)(base_t + c));
+                rp = OP::template identity<T>();
+                break;
+            }
+            __nanosleep(64);
+            S::load(rnd, r - 1, w);
+        }
+        has = true;
+    } else if (carry_in != nullptr) {
+        rp = *carry_in;
+        has = true;
+    }
+    if (c > 0) {
+        prefix = has ? OP::apply(rp, asum) : asum;
+        return true;
+    }
+    prefix = rp;
+    return has;
+}
+
+template <typename T, typename OP, int THREADS, int TILE_BYTES, bool EXCL>
+__global__ void __launch_bounds__(THREADS, 1) scan_generic_kernel(const ScanParams p) {
+    constexpr int NWARPS = THREADS / 32;
+    constexpr int V = TILE_BYTES / THREADS / 16;    // 16-byte vectors per thread
+    constexpr int ITEMS = V * 16 / (int)sizeof(T);  // elements per thread
+    constexpr int TILE_ELEMS = TILE_BYTES / (int)sizeof(T);
+    static_assert(V >= 1 && (V & (V - 1)) == 0, "vectors per thread must be a power of two");
+    static_assert(NWARPS <= 32 && NWARPS >= 2, "2..32 warps");
+    using S = Slot<T>;
+    const T ident = OP::template identity<T>();
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *st = smem;
+    T *warp_tot = reinterpret_cast<T *>(smem + TILE_BYTES);  // [NWARPS]
+    T *warp_exc = warp_tot + NWARPS;                        // [NWARPS]
+    T *tile_pre = warp_exc + NWARPS;                        // [1]
+    int *tile_has = reinterpret_cast<int *>(tile_pre + 1);  // [1]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t M = p.num_tiles;
+    Header *hdr = reinterpret_cast<Header *>(p.ws);
+    uint64_t *agg = reinterpret_cast<uint64_t *>(p.ws + kSlotBase);
+    uint64_t *rnd = agg + M * S::W;
+    const T *x = static_cast<const T *>(p.x);
+    T *y = static_cast<T *>(p.y);
+    const T *carry_in = static_cast<const T *>(p.carry_in);
+    const uint32_t tag = call_tag(hdr);
+    const int64_t my_tiles = (M - c + G - 1) / G;
+
+    for (int64_t k = 0; k < my_tiles; ++k) {
+        const int64_t t = c + k * G;
+        const int64_t t0 = t * TILE_ELEMS;
+        int64_t valid = p.n - t0;
+        if (valid > TILE_ELEMS) valid = TILE_ELEMS;
+        T *sv = reinterpret_cast<T *>(st);
+        for (int i = tid; i < TILE_ELEMS; i += THREADS) sv[i] = (i < valid) ? x[t0 + i] : ident;
+        __syncthreads();
+
+        Regs<T, V> r;
+        load_tile_regs<T, V>(st, tid, r);
+        T tsum = r.e[0];
+#pragma unroll
+        for (int i = 1; i < ITEMS; ++i) tsum = OP::apply(tsum, r.e[i]);
+        const T winc = warp_inclusive_scan<T, OP>(tsum, lane);
+        const T wexc = __shfl_up_sync(0xffffffffu, winc, 1);
+        if (lane == 31) warp_tot[warp] = winc;
+        __syncthreads();  // (A)
+
+        if (warp == 0) {
+            const T wt = lane < NWARPS ? warp_tot[lane] : ident;
+            const T wi = warp_inclusive_scan<T, OP>(wt, lane);
+            const T we = __shfl_up_sync(0xffffffffu, wi, 1);
+            const T tile_agg = __shfl_sync(0xffffffffu, wi, NWARPS - 1);
+            if (lane < NWARPS) warp_exc[lane] = we;
+            if (lane == 0) {
+                if (p.protocol_checks) {
+                    uint64_t w[S::W];
+                    T dummy;
+                    S::load(agg, t, w);
+                    if (S::decode(w, tag, dummy)) raise_error(hdr, 5u /*LS_ERR_PROTOCOL*/, (uint32_t)t);
+                }
+                if (t != p.stall_tile || p.spin_budget <= 0)
+                    S::publish(agg, t, tag, t == p.corrupt_tile ? ident : tile_agg);
+            }
+            T prefix = ident;
+            const bool has = (p.experiment & 1) ? false
+                                                : round_lookback<T, OP>(agg, rnd, k, c, G, tag, carry_in, lane,
+                                                                        p.spin_budget, hdr, prefix);
+            const T incl = has ? OP::apply(prefix, tile_agg) : tile_agg;
+            if (lane == 0) {
+                if (c == G - 1 && t + 1 < M) S::publish(rnd, k, tag, incl);
+                if (t == M - 1 && p.total_out != nullptr) *static_cast<T *>(p.total_out) = incl;
+                *tile_pre = prefix;
+                *tile_has = has ? 1 : 0;
+            }
+        }
+        __syncthreads();  // (B)
+
+        bool has = *tile_has != 0;
+        T acc = *tile_pre;
+        if (warp > 0) { acc = has ? OP::apply(acc, warp_exc[warp]) : warp_exc[warp]; has = true; }
+        if (lane > 0) { acc = has ? OP::apply(acc, wexc) : wexc; has = true; }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const T v = r.e[i];
+            const bool first = (i == 0 && !has);
+            if (EXCL) {
+                r.e[i] = first ? ident : acc;
+                acc = first ? v : OP::apply(acc, v);
+            } else {
+                acc = first ? v : OP::apply(acc, v);
+                r.e[i] = acc;
+            }
+        }
+        store_tile_regs<T, V>(st, tid, r);
+        __syncthreads();
+        for (int i = tid; i < valid; i += THREADS) y[t0 + i] = sv[i];
+        __syncthreads();  // the tile buffer is reused by the next iteration
+    }
+    __syncthreads();
+    if (tid == 0) epoch_handover(hdr, tag, G);
+}
+
+template <typename T, int THREADS, int TILE_BYTES>
+constexpr size_t scan_generic_smem_bytes() {
+    return (size_t)TILE_BYTES + (size_t)(2 * (THREADS / 32) + 1) * sizeof(T) + 16;
+}
+
+// ------------------------------------------------------------------------------
+// Deterministic grid reduction (the per-shard total for the multi-GPU carry
+// exchange): thread-serial over a fixed grid-stride partition, fixed warp and
+// block trees, the last CTA folds the per-CTA partials in index order.
+template <typename T, typename OP, int THREADS>
+__global__ void __launch_bounds__(THREADS) reduce_kernel(const T *__restrict__ x, int64_t n, T *total_out,
+                                                         uint8_t *ws) {
+    constexpr int NWARPS = THREADS / 32;
+    constexpr int PER_VEC = 16 / (int)sizeof(T);
+    __shared__ T wsum[NWARPS];
+    __shared__ bool last;
+    Header *hdr = reinterpret_cast<Header *>(ws);
+    T *partials = reinterpret_cast<T *>(ws + sizeof(Header));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t gtid = (int64_t)blockIdx.x * THREADS + tid;
+    const int64_t gstride = (int64_t)gridDim.x * THREADS;
+    const T ident = OP::template identity<T>();
+
+    const int64_t mis = (int64_t)(((uintptr_t)x & 15u) / sizeof(T));
+    int64_t head = mis ? (PER_VEC - mis) : 0;
+    if (head > n) head = n;
+    const int64_t nvec = (n - head) / PER_VEC;
+    const int64_t tail0 = head + nvec * PER_VEC;
+    T acc = ident;
+    if (gtid < head) acc = x[gtid];
+    const uint4 *xv = reinterpret_cast<const uint4 *>(x + head);
+    int64_t i = gtid;
+    for (; i + 3 * gstride < nvec; i += 4 * gstride) {
+        Regs<T, 4> q;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q.q[u] = __ldcs(xv + i + u * gstride);
+#pragma unroll
+        for (int j = 0; j < 4 * PER_VEC; ++j) acc = OP::apply(acc, q.e[j]);
+    }
+    for (; i < nvec; i += gstride) {
+        Regs<T, 1> q;
+        q.q[0] = __ldcs(xv + i);
+#pragma unroll
+        for (int j = 0; j < PER_VEC; ++j) acc = OP::apply(acc, q.e[j]);
+    }
+    if (gtid < n - tail0) acc = OP::apply(acc, x[tail0 + gtid]);
+
+    acc = warp_reduce_fixed<T, OP>(acc);
+    if (lane == 0) wsum[warp] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        T v = lane < NWARPS ? wsum[lane] : ident;
+        v = warp_reduce_fixed<T, OP>(v);
+        if (lane == 0) {
+            partials[blockIdx.x] = v;
+            __threadfence();
+            const uint32_t old = atom_add_acqrel_u32(&hdr->done, 1u);
+            last = (old == gridDim.x - 1u);
+        }
+    }
+    __syncthreads();
+    if (last && warp == 0) {
+        __threadfence();
+        T v = ident;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v = OP::apply(v, *((volatile T *)&partials[b]));
+        v = warp_reduce_fixed<T, OP>(v);
+        if (lane == 0) {
+            *total_out = v;
+            st_relaxed_u32(&hdr->done, 0u);
+        }
+    }
+}
+
+// carry_out = totals[0] (+) ... (+) totals[rank-1]  (fixed left fold)
+template <typename T, typename OP>
+__global__ void carry_kernel(const T *totals, int64_t rank, T *carry_out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        T acc = OP::template identity<T>();
+        if (rank > 0) acc = totals[0];
+        for (int64_t g = 1; g < rank; ++g) acc = OP::apply(acc, totals[g]);
+        *carry_out = acc;
+    }
+}
+
+}  // namespace lscan

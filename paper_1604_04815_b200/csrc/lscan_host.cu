@@ -122,9 +122,9 @@ int esize(ls_dtype dt) { return (dt == LS_I32 || dt == LS_F32) ? 4 : 8; }
 
 }  // namespace
 
-extern "C" ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
-                                           int device) {
-    if (dt < LS_I32 || dt > LS_F64) return LS_ERR_UNSUPPORTED_DTYPE;
+extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
+                                  int device) {
+    if (dt < LS_I32 || dt > LS_F64 || op < LS_OP_ADD || op > LS_OP_MIN) return LS_ERR_UNSUPPORTED_DTYPE;
     if (n < 0 || (n > 0 && (!x || !y))) return LS_ERR_INVALID_ARG;
     if (n == 0) return LS_OK;
     const int es = esize(dt);
@@ -180,8 +180,8 @@ extern "C" ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, 
         HC(cudaStreamWaitEvent(c->s_comp, c->ev_in[b], 0), "wait copy-in");
         const void *cin = k ? carry + 16 * ((k - 1) & 1) : nullptr;
         void *cout = carry + 16 * (k & 1);
-        st = exclusive ? ls_exclusive_sum(dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp)
-                       : ls_inclusive_sum(dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp);
+        st = exclusive ? ls_exclusive_scan(op, dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp)
+                       : ls_inclusive_scan(op, dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp);
         if (st != LS_OK) return st;
         HC(cudaEventRecord(c->ev_comp[b], c->s_comp), "event");
         HC(cudaStreamWaitEvent(c->s_out, c->ev_comp[b], 0), "wait scan");
@@ -197,4 +197,9 @@ extern "C" ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, 
     HC(cudaStreamSynchronize(c->s_comp), "final sync");
     if (prev != dev) HC(cudaSetDevice(prev), "cudaSetDevice");
     return LS_OK;
+}
+
+extern "C" ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
+                                           int device) {
+    return ls_scan_host(LS_OP_ADD, dt, x, y, n, exclusive, device);
 }

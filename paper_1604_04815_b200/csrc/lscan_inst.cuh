@@ -1,0 +1,62 @@
+// lscan_inst.cuh — builds the DtypeKernels table for one element type
+// (included by exactly one lscan_inst_<dtype>.cu each).
+#pragma once
+#include "lscan_dispatch.h"
+#include "lscan_generic.cuh"
+#include "lscan_scan_ws2.cuh"
+
+namespace lscan {
+
+template <typename T, typename OP, bool EXCL>
+Launch fast_launch() {
+    using C = FastCfg<sizeof(T)>;
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL>, (C::kScanWarps + 3) * 32,
+            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(), C::kTileBytes, C::kStages};
+}
+
+template <typename T, typename OP, bool EXCL>
+Launch generic_launch() {
+    return {&scan_generic_kernel<T, OP, kGenThreads, kGenTileBytes, EXCL>, kGenThreads,
+            scan_generic_smem_bytes<T, kGenThreads, kGenTileBytes>(), kGenTileBytes, 1};
+}
+
+template <typename T, typename OP>
+void fill_op(DtypeKernels &k) {
+    k.scan[OP::code][0][1] = fast_launch<T, OP, false>();
+    k.scan[OP::code][1][1] = fast_launch<T, OP, true>();
+    k.scan[OP::code][0][0] = generic_launch<T, OP, false>();
+    k.scan[OP::code][1][0] = generic_launch<T, OP, true>();
+    k.reduce_fn[OP::code] = (const void *)&reduce_kernel<T, OP, kReduceThreads>;
+}
+
+template <typename T>
+void launch_reduce_t(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s) {
+    const T *xp = static_cast<const T *>(x);
+    T *tp = static_cast<T *>(total_out);
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    if (op == OpMax::code) reduce_kernel<T, OpMax, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+    else if (op == OpMin::code) reduce_kernel<T, OpMin, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+    else reduce_kernel<T, OpAdd, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+}
+
+template <typename T>
+void launch_carry_t(int op, const void *totals, int64_t rank, void *carry_out, cudaStream_t s) {
+    const T *tp = static_cast<const T *>(totals);
+    T *cp = static_cast<T *>(carry_out);
+    if (op == OpMax::code) carry_kernel<T, OpMax><<<1, 32, 0, s>>>(tp, rank, cp);
+    else if (op == OpMin::code) carry_kernel<T, OpMin><<<1, 32, 0, s>>>(tp, rank, cp);
+    else carry_kernel<T, OpAdd><<<1, 32, 0, s>>>(tp, rank, cp);
+}
+
+template <typename T>
+DtypeKernels make_kernels() {
+    DtypeKernels k{};
+    fill_op<T, OpAdd>(k);
+    fill_op<T, OpMax>(k);
+    fill_op<T, OpMin>(k);
+    k.launch_reduce = &launch_reduce_t<T>;
+    k.launch_carry = &launch_carry_t<T>;
+    return k;
+}
+
+}  // namespace lscan

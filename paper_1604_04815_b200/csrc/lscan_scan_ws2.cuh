@@ -1,28 +1,34 @@
-// lscan_scan_ws2.cuh — warp-specialised persistent scan, register-resident
-// results (the hot path).
+// lscan_scan_ws2.cuh — the hot path: warp-specialised persistent single-pass
+// scan with register-resident results, for 16-byte-aligned x and y.
 //
-// Differs from scan_ws_kernel (lscan_scan_ws.cuh) in where a tile lives
-// after it lands: the scanner warps copy it from the shared-memory stage
-// into registers in the paper's lane-strided layout (Alg. 2,
-// PAPER.md:137-189; warp.py:85-90 regs[j, i] = tile[i + W*j], here with
-// 16-byte vectors as the "element" of a row) and release the stage at once,
-// so the TMA ring holds only data in flight — not tiles waiting for their
-// prefix.  Results go from registers straight to y with coalesced 128-bit
-// stores (each warp instruction covers 512 contiguous bytes).
+// Maps the reference's chained pipeline (chainscan/chained.py:316-357) onto
+// a B200.  The roles the reference's worker performs in sequence per block
+// (chained.py:237-249: local accumulate -> inter_block_comm -> combine) run
+// as concurrent warp roles inside each persistent CTA, so the cross-CTA carry
+// chain is resolved ahead of the data pass instead of stalling it:
 //
-//   producer warp   TMA bulk loads into a STAGES-deep ring; a stage is
-//                   refilled as soon as the scanners and the reducer have
-//                   read it
-//   reducer warp    sums each landed tile, publishes A[t] (never waits on
-//                   another CTA)
-//   look-back warp  prefix(t) = R[r-1] (+) A[rG..rG+c-1] into a smem ring;
-//                   CTA G-1 also publishes R[r] (the only serial chain)
-//   scanner warps   V rows per warp: thread-serial fold of each 16-byte
-//                   vector, __shfl_up_sync row scan, serial row carry
-//                   (Alg. 2), smem scan of warp totals (Alg. 3), prefix fold
-//                   and store (Alg. 5)
+//   producer warp   1-D TMA bulk loads (cp.async.bulk) of whole tiles into a
+//                   STAGES-deep shared-memory ring; a stage is refilled as
+//                   soon as the scanners and the reducer have read it
+//   reducer warp    reduces each landed tile and publishes A[t] (never waits
+//                   on another CTA)
+//   look-back warp  prefix(t) = R[r-1] (+) A[rG] (+) ... (+) A[rG+c-1] into a
+//                   shared-memory ring; CTA G-1 also publishes the round
+//                   prefix R[r] = prefix(t) (+) A[t] (the only serial chain:
+//                   one L2 round trip per round of G tiles)
+//   scanner warps   copy the tile into registers in the paper's lane-strided
+//                   layout (Alg. 2, warp.py:85-90, with
+//                   16-byte vectors as row elements) and release the stage;
+//                   thread-serial fold per vector, __shfl_up_sync row scan and
+//                   serial row carry (Alg. 2), shared-memory scan of warp
+//                   totals (Alg. 3), prefix fold (Alg. 5), coalesced STG.128
+//
+// Tile t = r*G + c is CTA c's r-th tile: cyclic, ascending, no atomic ticket
+// (Alg. 1; chained.py:270).  The launch is cooperative, so the driver refuses
+// a grid that cannot be co-resident.  Sums are fixed-order:
+// results depend on (n, G, tile shape) only, never on timing.
 #pragma once
-#include "lscan_scan_ws.cuh"
+#include "lscan_common.cuh"
 
 namespace lscan {
 
@@ -31,7 +37,109 @@ __device__ __forceinline__ void stg128(void *p, uint4 v) {
                  : "memory");
 }
 
-template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL>
+// reduce a whole shared-memory tile with one warp (lane-strided 16-byte
+// vectors, conflict-free), four independent accumulators, fixed order
+template <typename T, typename OP, int TILE_BYTES>
+__device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
+    constexpr int NV = TILE_BYTES / 16 / 32;  // 16-byte vectors per lane
+    constexpr int PER = 16 / (int)sizeof(T);
+    static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
+    const T ident = OP::template identity<T>();
+    T acc[4] = {ident, ident, ident, ident};
+    const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
+#pragma unroll 2
+    for (int j = 0; j < NV; j += 4) {
+        Regs<T, 4> r;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r.q[u] = lds128(base + (uint32_t)(j + u) * 512u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int e = 0; e < PER; ++e) acc[u] = OP::apply(acc[u], r.e[u * PER + e]);
+    }
+    return warp_reduce_fixed<T, OP>(OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3])));
+}
+
+template <typename T>
+struct LookbackOut {
+    T r;    // R[k-1]
+    T sum;  // A[kG] (+) ... (+) A[kG+c-1]
+    T own;  // A[t]
+};
+
+// One look-back step for tile t = k*G + c, every load in flight at once: the
+// round prefix R[k-1] (when need_r), the aggregates A[kG .. kG+c-1] and, when
+// want_own, A[t] itself.  Spins (with nanosleep back-off) until every word
+// carries `tag`; a spin budget turns a stall into LS_ERR_LIVENESS.
+template <typename T, typename OP>
+__device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, const uint64_t *rnd, int64_t k, int c,
+                                                       int G, bool need_r, bool want_own, uint32_t tag, int lane,
+                                                       int64_t spin_budget, Header *hdr, uint32_t where) {
+    using S = Slot<T>;
+    constexpr int U = 5;  // 160 slots per pass covers a 148-SM round
+    const T ident = OP::template identity<T>();
+    const int count = c + (want_own ? 1 : 0);
+    const int64_t first = k * (int64_t)G;
+    T acc = ident, own = ident, r = ident;
+    int64_t probes = 0;
+    bool r_pending = need_r;
+    uint64_t rw[S::W];
+    if (need_r) S::load(rnd, k - 1, rw);
+    for (int base = 0; base < count || r_pending; base += 32 * U) {
+        uint64_t w[U][S::W];
+        bool need[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * 32 + lane;
+            need[u] = j < count;
+            if (need[u]) S::load(agg, first + j, w[u]);
+        }
+        T val[U];
+        while (true) {
+            bool ok = true;
+            if (r_pending) {
+                if (S::decode(rw, tag, r)) r_pending = false;
+                else ok = false;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (need[u]) {
+                    if (S::decode(w[u], tag, val[u])) need[u] = false;
+                    else ok = false;
+                }
+            }
+            if (__all_sync(0xffffffffu, ok)) break;
+            if (spin_budget > 0 && ++probes > spin_budget) {
+                if (lane == 0) raise_error(hdr, 4u /*LS_ERR_LIVENESS*/, where);
+                if (r_pending) { r = ident; r_pending = false; }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (need[u]) { val[u] = ident; need[u] = false; }
+                break;
+            }
+            __nanosleep(32);
+            if (r_pending) S::load(rnd, k - 1, rw);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = base + u * 32 + lane;
+                if (need[u]) S::load(agg, first + j, w[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * 32 + lane;
+            if (j < c) acc = OP::apply(acc, val[u]);
+            else if (j == c && want_own) own = val[u];
+        }
+    }
+    LookbackOut<T> o;
+    o.sum = warp_reduce_fixed<T, OP>(acc);
+    o.r = r;
+    o.own = want_own ? __shfl_sync(0xffffffffu, own, c & 31) : ident;
+    return o;
+}
+
+template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL>
 __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(const ScanParams p) {
     constexpr int SCAN_THREADS = SCAN_WARPS * 32;
     constexpr int V = TILE_BYTES / SCAN_THREADS / 16;  // rows (16-byte vectors) per lane
@@ -39,15 +147,16 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
     constexpr int TILE_ELEMS = TILE_BYTES / (int)sizeof(T);
     constexpr int WARP_BYTES = TILE_BYTES / SCAN_WARPS;
     constexpr int W_PROD = SCAN_WARPS, W_RED = SCAN_WARPS + 1, W_AUX = SCAN_WARPS + 2;
-    static_assert(V >= 1, "at least one row per lane");
+    static_assert(V >= 1 && TILE_BYTES % (SCAN_THREADS * 16) == 0, "whole rows per lane");
     static_assert(SCAN_WARPS >= 2 && SCAN_WARPS + 3 <= 32, "2..29 scanner warps");
     using S = Slot<T>;
+    const T ident = OP::template identity<T>();
 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stages = smem;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * TILE_BYTES);  // data landed
-    uint64_t *empty = full + STAGES;      // scanners + reducer done reading (2 arrivals)
-    uint64_t *pre_ready = empty + STAGES; // prefix written
+    uint64_t *empty = full + STAGES;          // scanners + reducer done reading (2 arrivals)
+    uint64_t *pre_ready = empty + STAGES;     // prefix written
     uint64_t *pre_free = pre_ready + STAGES;  // prefix consumed
     T *pre = reinterpret_cast<T *>(pre_free + STAGES);
     int *pre_has = reinterpret_cast<int *>(pre + STAGES);
@@ -62,9 +171,7 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
     uint64_t *rnd = agg + M * S::W;
     const T *x = static_cast<const T *>(p.x);
     T *y = static_cast<T *>(p.y);
-
-    const uint32_t prev_epoch = ld_relaxed_u32(&hdr->epoch);
-    const uint32_t tag = (prev_epoch + 1u) == 0u ? 1u : prev_epoch + 1u;
+    const uint32_t tag = call_tag(hdr);
     const int64_t my_tiles = (M - c + G - 1) / G;
     const int64_t full_tiles = p.n / TILE_ELEMS;
 
@@ -87,27 +194,28 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
             const int64_t t0 = t * TILE_ELEMS;
+            uint8_t *sb = stages + s * TILE_BYTES;
             if (t < full_tiles) {
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[s], TILE_BYTES);
-                    tma_load_1d(stages + s * TILE_BYTES, x + t0, TILE_BYTES, &full[s], pol);
+                    tma_load_1d(sb, x + t0, TILE_BYTES, &full[s], pol);
                 }
             } else {
-                // partial_tail (chained.py:188-202): the 16-byte-aligned prefix of
-                // the last tile by TMA, the ragged vector by plain loads, the rest
-                // of the stage identity-filled with 128-bit shared stores
+                // partial_tail (chained.py:188-202): the 16-byte-aligned prefix
+                // by TMA, the ragged vector by plain loads, the rest of the
+                // stage identity-filled with 128-bit shared stores
                 const int64_t valid = p.n - t0;
                 const uint32_t bulk = (uint32_t)((valid * (int64_t)sizeof(T)) & ~(int64_t)15);
                 const int vfirst = (int)(bulk / 16);  // first vector not covered by TMA
-                uint8_t *sb = stages + s * TILE_BYTES;
                 const uint32_t sbase = smem_u32(sb);
-                for (int v = vfirst + 1 + lane; v < TILE_BYTES / 16; v += 32) sts128(sbase + (uint32_t)v * 16u, make_uint4(0, 0, 0, 0));
-                if (lane == 0 && vfirst < TILE_BYTES / 16) {
+                const uint4 iv = identity_vec<T, OP>();
+                for (int v = vfirst + 1 + lane; v < TILE_BYTES / 16; v += 32) sts128(sbase + (uint32_t)v * 16u, iv);
+                if (lane == 0) {
                     Regs<T, 1> rv;
 #pragma unroll
                     for (int e = 0; e < PER; ++e) {
                         const int64_t i = (int64_t)vfirst * PER + e;
-                        rv.e[e] = i < valid ? x[t0 + i] : T(0);
+                        rv.e[e] = i < valid ? x[t0 + i] : ident;
                     }
                     sts128(sbase + (uint32_t)vfirst * 16u, rv.q[0]);
                 }
@@ -134,7 +242,7 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
             const int64_t t = c + k * G;
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
             if (p.delay_red_ns > 0 && t % 3 == 1) debug_sleep(p.delay_red_ns);
-            const T a = reduce_stage<T, TILE_BYTES>(stages + s * TILE_BYTES, lane);
+            const T a = reduce_stage<T, OP, TILE_BYTES>(stages + s * TILE_BYTES, lane);
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&empty[s]);
@@ -144,21 +252,23 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
                     S::load(agg, t, w);
                     if (S::decode(w, tag, dummy)) raise_error(hdr, 5u /*LS_ERR_PROTOCOL*/, (uint32_t)t);
                 }
-                if (t != p.stall_tile || p.spin_budget <= 0) S::publish(agg, t, tag, t == p.corrupt_tile ? T(0) : a);
+                if (t != p.stall_tile || p.spin_budget <= 0) S::publish(agg, t, tag, t == p.corrupt_tile ? ident : a);
             }
         }
     } else if (warp == W_AUX) {
         // ----------------------------------------------------------- look-back
         const T *carry_in = static_cast<const T *>(p.carry_in);
         const bool have_carry = carry_in != nullptr;
-        T r_prev = have_carry ? *carry_in : T(0);
+        T r_prev = have_carry ? *carry_in : ident;  // R[k-1] as known to CTA G-1 (the chain owner)
         for (int64_t k = 0; k < my_tiles; ++k) {
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
             const bool chain = (c == G - 1) && (t + 1 < M);
+            // R[k-1]: the caller's carry in round 0, the chain owner's register,
+            // or the published round slot for everyone else
             const bool need_r = k > 0 && c != G - 1;
-            const LookbackOut<T> lb = aux_lookback<T>(agg, rnd, k, c, G, need_r, chain, tag, lane, p.spin_budget,
-                                                      hdr, (uint32_t)t);
+            const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, chain, tag, lane,
+                                                          p.spin_budget, hdr, (uint32_t)t);
             bool has;
             T base;
             if (k == 0) { has = have_carry; base = r_prev; }
@@ -166,11 +276,11 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
             else { has = true; base = lb.r; }
             T prefix = base;
             if (c > 0) {
-                prefix = has ? (base + lb.sum) : lb.sum;
+                prefix = has ? OP::apply(base, lb.sum) : lb.sum;
                 has = true;
             }
             if (chain) {
-                r_prev = has ? (prefix + lb.own) : lb.own;
+                r_prev = has ? OP::apply(prefix, lb.own) : lb.own;  // R[k]
                 if (lane == 0) S::publish(rnd, k, tag, r_prev);
             }
             if (k >= STAGES) mbar_wait(&pre_free[s], (uint32_t)(((k - STAGES) / STAGES) & 1));
@@ -194,26 +304,26 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
             const uint32_t sbase = smem_u32(stages + s * TILE_BYTES) + wbase;
 #pragma unroll
             for (int j = 0; j < V; ++j) r.q[j] = lds128(sbase + (uint32_t)j * 512u);
-            // per row: lane-serial sum of the vector, inclusive warp scan of those
-            T rex[V];  // exclusive prefix of this lane within row j (valid for lane > 0)
+            // per row j: lane-serial fold of the vector, inclusive warp scan
+            T rex[V];   // exclusive prefix of this lane within row j (lane > 0)
             T rtot[V];  // row totals
 #pragma unroll
             for (int j = 0; j < V; ++j) {
                 T v = r.e[j * PER];
 #pragma unroll
-                for (int e = 1; e < PER; ++e) v = v + r.e[j * PER + e];
-                const T inc = warp_inclusive_scan(v, lane);
+                for (int e = 1; e < PER; ++e) v = OP::apply(v, r.e[j * PER + e]);
+                const T inc = warp_inclusive_scan<T, OP>(v, lane);
                 rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
                 rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
             }
-            // serial row carry (Alg. 2): running prefix of the rows before j
+            // serial row carry (Alg. 2): prefix of the rows before j
             T rowpre[V];
             T run = rtot[0];
-            rowpre[0] = T(0);
+            rowpre[0] = ident;
 #pragma unroll
             for (int j = 1; j < V; ++j) {
                 rowpre[j] = run;
-                run = run + rtot[j];
+                run = OP::apply(run, rtot[j]);
             }
             if (lane == 0) warp_tot[warp] = run;
             named_bar_sync(1, SCAN_THREADS);  // (A) stage fully read; warp totals visible
@@ -222,23 +332,23 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
                 if (k > 0) mbar_arrive(&pre_free[(k - 1) % STAGES]);
             }
             if (warp == 0) {
-                const T wt = lane < SCAN_WARPS ? warp_tot[lane] : T(0);
-                const T wi = warp_inclusive_scan(wt, lane);
+                const T wt = lane < SCAN_WARPS ? warp_tot[lane] : ident;
+                const T wi = warp_inclusive_scan<T, OP>(wt, lane);
                 const T we = __shfl_up_sync(0xffffffffu, wi, 1);
                 if (lane < SCAN_WARPS) warp_exc[lane] = we;
                 if (t == M - 1 && p.total_out != nullptr) {
                     mbar_wait(&pre_ready[s], parity);
                     const T blk = __shfl_sync(0xffffffffu, wi, SCAN_WARPS - 1);
-                    if (lane == 0) *static_cast<T *>(p.total_out) = pre_has[s] ? (pre[s] + blk) : blk;
+                    if (lane == 0) *static_cast<T *>(p.total_out) = pre_has[s] ? OP::apply(pre[s], blk) : blk;
                 }
             }
             mbar_wait(&pre_ready[s], parity);
             named_bar_sync(1, SCAN_THREADS);  // (B)
-            // carry into this lane's first element of each row:
+            // carry into the first element of each of this lane's rows:
             //   tile prefix (+) warps before (+) rows before (+) lanes before
             bool has0 = pre_has[s] != 0;
             T wcarry = pre[s];
-            if (warp > 0) { wcarry = has0 ? (wcarry + warp_exc[warp]) : warp_exc[warp]; has0 = true; }
+            if (warp > 0) { wcarry = has0 ? OP::apply(wcarry, warp_exc[warp]) : warp_exc[warp]; has0 = true; }
             T *yt = y + t * (int64_t)TILE_ELEMS;
             const bool partial = t >= full_tiles;
             const int64_t valid = p.n - t * (int64_t)TILE_ELEMS;
@@ -246,16 +356,17 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
             for (int j = 0; j < V; ++j) {
                 bool has = has0;
                 T acc = wcarry;
-                if (j > 0) { acc = has ? (acc + rowpre[j]) : rowpre[j]; has = true; }
-                if (lane > 0) { acc = has ? (acc + rex[j]) : rex[j]; has = true; }
+                if (j > 0) { acc = has ? OP::apply(acc, rowpre[j]) : rowpre[j]; has = true; }
+                if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
 #pragma unroll
                 for (int e = 0; e < PER; ++e) {
                     const T v = r.e[j * PER + e];
+                    const bool first = (e == 0 && !has);
                     if (EXCL) {
-                        r.e[j * PER + e] = (e == 0 && !has) ? T(0) : acc;
-                        acc = (e == 0 && !has) ? v : (acc + v);
+                        r.e[j * PER + e] = first ? ident : acc;
+                        acc = first ? v : OP::apply(acc, v);
                     } else {
-                        acc = (e == 0 && !has) ? v : (acc + v);
+                        acc = first ? v : OP::apply(acc, v);
                         r.e[j * PER + e] = acc;
                     }
                 }
@@ -272,18 +383,13 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
     }
 
     __syncthreads();
-    if (tid == 0) {
-        const uint32_t old = atom_add_acqrel_u32(&hdr->done, 1u);
-        if (old == (uint32_t)G - 1u) {
-            st_relaxed_u32(&hdr->done, 0u);
-            st_relaxed_u32(&hdr->epoch, tag);
-        }
-    }
+    if (tid == 0) epoch_handover(hdr, tag, G);
 }
 
 template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES>
 constexpr size_t scan_ws2_smem_bytes() {
-    return scan_ws_smem_bytes<T, SCAN_WARPS, TILE_BYTES, STAGES>();
+    return (size_t)STAGES * TILE_BYTES + 4 * STAGES * 8 + STAGES * sizeof(T) + (STAGES + 1) * 4 +
+           2 * SCAN_WARPS * sizeof(T) + 32;
 }
 
 }  // namespace lscan

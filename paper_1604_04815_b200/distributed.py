@@ -47,22 +47,24 @@ class ShardOps:
     scan: Callable[..., torch.Tensor]  # (shard, carry, exclusive, out=None) -> scanned shard
 
 
-def cuda_ops() -> ShardOps:
+def cuda_ops(op: str = "add") -> ShardOps:
     from . import scan as S
 
     def _scan(x, carry, exclusive, out=None):
-        return (S.exclusive_scan if exclusive else S.inclusive_scan)(x, out, carry_in=carry)
+        return (S.exclusive_scan if exclusive else S.inclusive_scan)(x, out, carry_in=carry, op=op)
 
-    return ShardOps(reduce=S.reduce_sum, carry=S.carry_from_totals, scan=_scan)
+    return ShardOps(reduce=lambda x: S.reduce(x, op=op),
+                    carry=lambda t, r: S.carry_from_totals(t, r, op=op), scan=_scan)
 
 
 def sharded_scan(shard: torch.Tensor, *, exclusive: bool = False, group=None,
-                 ops: Optional[ShardOps] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 ops: Optional[ShardOps] = None, out: Optional[torch.Tensor] = None,
+                 op: str = "add") -> torch.Tensor:
     """Scan this rank's shard as part of the global array (ranks in order).
 
     Every rank must call this collectively.  Returns this rank's slice of the
     global scan."""
-    ops = ops or cuda_ops()
+    ops = ops or cuda_ops(op)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     total = ops.reduce(shard).reshape(1)

@@ -3,10 +3,9 @@
 Mirrors ``chainscan.operators`` (operators.py:24-127): the same dtype tokens,
 the same ``make_operator(name, elem_type)`` factory and error class, and an
 operator object exposing ``name``, ``dtype`` and ``identity``.  The device
-path implements ``add`` (the north-star operator); ``max``/``min`` objects
-can be built (the reference's operator table) but the scan entry points
-reject them with ``UnsupportedOperatorError`` instead of silently running
-something else.
+kernels implement all three operators of the reference's table: ``add`` (the
+north-star operator), ``max`` and ``min``; float max/min propagate NaN like
+``np.maximum`` / ``np.minimum``.
 
 Integer add wraps modulo 2^width (two's complement), as the reference's
 ``np.add`` under ``errstate(over="ignore")`` does (operators.py:74-100).
@@ -27,7 +26,7 @@ DTYPES = {
 }
 
 OPERATOR_NAMES = ("add", "max", "min")
-DEVICE_OPERATORS = ("add",)
+DEVICE_OPERATORS = ("add", "max", "min")
 
 
 class UnsupportedOperatorError(ValueError):
@@ -88,7 +87,7 @@ def make_operator(name: str, elem_type) -> ScanOperator:
 
 
 def require_device_operator(op) -> np.dtype:
-    """The device path computes ``add`` only; anything else is rejected."""
+    """The operator must be one the device implements (add / max / min)."""
     name = getattr(op, "name", None)
     if name not in DEVICE_OPERATORS:
         raise UnsupportedOperatorError(

@@ -78,9 +78,18 @@ def _scalar_ptr(t: Optional[torch.Tensor], like: torch.Tensor, what: str) -> Opt
     return t.data_ptr()
 
 
-def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exclusive: bool) -> torch.Tensor:
+def op_code(op: str) -> int:
+    try:
+        return N.OPS[op]
+    except KeyError:
+        raise UnsupportedOperatorError(f"unknown operator {op!r}; supported: {', '.join(N.OPS)}") from None
+
+
+def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exclusive: bool,
+          op: str = "add") -> torch.Tensor:
     _check_1d(x)
     dt = dtype_code(x.dtype)
+    oc = op_code(op)
     if out is None:
         out = torch.empty_like(x, memory_format=torch.contiguous_format)
     else:
@@ -97,9 +106,9 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
     stream = torch.cuda.current_stream(x.device)
     L = N.lib()
     ws = workspace(x.device, stream, L.ls_workspace_bytes(dt, n))
-    fn = L.ls_exclusive_sum if exclusive else L.ls_inclusive_sum
+    fn = L.ls_exclusive_scan if exclusive else L.ls_inclusive_scan
     with torch.cuda.device(x.device):
-        rc = fn(dt, x.data_ptr() if n else None, out.data_ptr() if n else None, n,
+        rc = fn(oc, dt, x.data_ptr() if n else None, out.data_ptr() if n else None, n,
                 _scalar_ptr(carry_in, x, "carry_in"), _scalar_ptr(total_out, x, "total_out"),
                 ws.data_ptr(), ws.numel(), stream.cuda_stream)
     raise_for_status(rc)
@@ -108,25 +117,27 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
 
 def inclusive_scan(x: torch.Tensor, out: Optional[torch.Tensor] = None, *,
                    carry_in: Optional[torch.Tensor] = None,
-                   total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                   total_out: Optional[torch.Tensor] = None, op: str = "add") -> torch.Tensor:
     """y[j] = carry (+) x[0] (+) ... (+) x[j] on the device; ``out`` may be ``x``.
 
-    ``carry_in`` / ``total_out`` are optional one-element device tensors of
-    x's dtype (the multi-GPU carry seam)."""
-    return _scan(x, out, carry_in, total_out, exclusive=False)
+    ``op`` is ``"add"`` (default), ``"max"`` or ``"min"``.  ``carry_in`` /
+    ``total_out`` are optional one-element device tensors of x's dtype (the
+    multi-GPU carry seam)."""
+    return _scan(x, out, carry_in, total_out, exclusive=False, op=op)
 
 
 def exclusive_scan(x: torch.Tensor, out: Optional[torch.Tensor] = None, *,
                    carry_in: Optional[torch.Tensor] = None,
-                   total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """y[0] = carry (identity), y[j] = carry (+) x[0] (+) ... (+) x[j-1]."""
-    return _scan(x, out, carry_in, total_out, exclusive=True)
+                   total_out: Optional[torch.Tensor] = None, op: str = "add") -> torch.Tensor:
+    """y[0] = carry (or the identity), y[j] = carry (+) x[0] (+) ... (+) x[j-1]."""
+    return _scan(x, out, carry_in, total_out, exclusive=True, op=op)
 
 
-def reduce_sum(x: torch.Tensor, total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """Deterministic device sum of x into a one-element tensor."""
+def reduce(x: torch.Tensor, total_out: Optional[torch.Tensor] = None, op: str = "add") -> torch.Tensor:
+    """Deterministic device reduction of x into a one-element tensor."""
     _check_1d(x)
     dt = dtype_code(x.dtype)
+    oc = op_code(op)
     if not x.is_contiguous():
         x = x.contiguous()
     if total_out is None:
@@ -135,22 +146,29 @@ def reduce_sum(x: torch.Tensor, total_out: Optional[torch.Tensor] = None) -> tor
     L = N.lib()
     ws = workspace(x.device, stream, L.ls_workspace_bytes(dt, 0))
     with torch.cuda.device(x.device):
-        rc = L.ls_reduce_sum(dt, x.data_ptr() if x.numel() else None, x.numel(),
+        rc = L.ls_reduce(oc, dt, x.data_ptr() if x.numel() else None, x.numel(),
                              _scalar_ptr(total_out, x, "total_out"), ws.data_ptr(), ws.numel(),
                              stream.cuda_stream)
     raise_for_status(rc)
     return total_out
 
 
-def carry_from_totals(totals: torch.Tensor, rank: int, carry_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+def reduce_sum(x: torch.Tensor, total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Deterministic device sum of x into a one-element tensor."""
+    return reduce(x, total_out, op="add")
+
+
+def carry_from_totals(totals: torch.Tensor, rank: int, carry_out: Optional[torch.Tensor] = None,
+                      op: str = "add") -> torch.Tensor:
     """carry = totals[0] (+) ... (+) totals[rank-1] on the device (fixed order)."""
     _check_1d(totals, "totals")
     dt = dtype_code(totals.dtype)
+    oc = op_code(op)
     if carry_out is None:
         carry_out = torch.empty(1, dtype=totals.dtype, device=totals.device)
     stream = torch.cuda.current_stream(totals.device)
     with torch.cuda.device(totals.device):
-        rc = N.lib().ls_carry_from_totals(dt, totals.data_ptr(), totals.numel(), rank,
+        rc = N.lib().ls_carry_from_totals(oc, dt, totals.data_ptr(), totals.numel(), rank,
                                          carry_out.data_ptr(), stream.cuda_stream)
     raise_for_status(rc)
     return carry_out

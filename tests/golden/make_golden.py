@@ -66,6 +66,14 @@ def main() -> int:
                 arrays[f"x_{key}"] = x
                 arrays[f"seq_{key}"] = y
                 arrays[f"chained_{key}"] = yc
+    # max / min through the reference's oracle (test_acceptance.py:55-82 uses add and max)
+    for tok in TOKS:
+        for name in ("max", "min"):
+            op = cs.make_operator(name, tok)
+            for n in (1, 7, 33, 1000, 8193):
+                x = cs.generate_input(n, tok, [5, n])
+                arrays[f"x_{name}_{tok}_n{n}"] = x
+                arrays[f"seq_{name}_{tok}_n{n}"] = cs.sequential_scan(cs.ScanProblem(x, op))
     # corrupt-slot red path (test_chained.py:275-284): B=2, L=16, ones(64) i64
     op = cs.make_operator("add", "i64")
     ones = np.ones(64, dtype=np.int64)

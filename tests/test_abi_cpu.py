@@ -68,7 +68,9 @@ def test_argument_checks_without_launch():
     assert "overlap" in N.last_detail()
     # misaligned element pointer
     assert lib.ls_inclusive_sum(N.LS_I32, base + 1, base + 129, 4, None, None, None, 0, None) == N.LS_ERR_INVALID_ARG
-    assert lib.ls_carry_from_totals(N.LS_I32, None, 4, 0, None, None) == N.LS_ERR_INVALID_ARG
+    assert lib.ls_carry_from_totals(N.LS_OP_ADD, N.LS_I32, None, 4, 0, None, None) == N.LS_ERR_INVALID_ARG
+    assert lib.ls_inclusive_scan(7, N.LS_I32, None, None, 1, None, None, None, 0, None) == N.LS_ERR_UNSUPPORTED_DTYPE
+    assert lib.ls_reduce(N.LS_OP_MAX, 9, None, 1, None, None, 0, None) == N.LS_ERR_UNSUPPORTED_DTYPE
     assert lib.ls_debug_config(0, -1, 0) == 0
 
 
@@ -100,9 +102,12 @@ def test_problem_and_config_validation():
 
 def test_drop_in_rejects_before_device():
     x = np.arange(10, dtype=np.int32)
-    for name in ("max", "min"):
-        with pytest.raises(P.UnsupportedOperatorError):
-            P.chained_scan(P.ScanProblem(x, P.make_operator(name, "i32")))
+
+    class Xor:  # an operator the device does not implement
+        name, dtype, identity = "xor", np.dtype(np.int32), 0
+
+    with pytest.raises(P.UnsupportedOperatorError):
+        P.chained_scan(P.ScanProblem(x, Xor()))
     with pytest.raises(P.ShapeError):  # dtype mismatch is refused, not guessed
         P.chained_scan(P.ScanProblem(x, P.make_operator("add", "i64")))
     # empty input: returns the output object untouched (chained.py:331-332)

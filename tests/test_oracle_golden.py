@@ -19,7 +19,25 @@ def sha16(a):
 
 
 def small_keys(golden):
-    return sorted(k[2:] for k in golden["arrays"] if k.startswith("x_"))
+    # add cases are keyed <tok>_s<seed>_n<n>; max/min cases <op>_<tok>_n<n>
+    return sorted(k[2:] for k in golden["arrays"] if k.startswith("x_") and k.split("_")[2].startswith("s"))
+
+
+def op_keys(golden):
+    return sorted(k[2:] for k in golden["arrays"] if k.startswith("x_") and k.split("_")[1] in ("max", "min"))
+
+
+def test_max_min_oracle_matches_reference(golden, oracle_lib):
+    keys = op_keys(golden)
+    assert len(keys) == 2 * 4 * 5
+    for key in keys:
+        name, tok, n = key.split("_")
+        x = golden["arrays"]["x_" + key]
+        assert np.array_equal(x, oracle_lib.generate_input(int(n[1:]), tok, [5, int(n[1:])]))
+        ref = golden["arrays"]["seq_" + key]
+        assert np.array_equal(oracle_lib.sequential_scan(x, op=name).view(np.uint8), ref.view(np.uint8)), key
+        ex = oracle_lib.exclusive_scan(x, name)
+        assert ex[0] == oracle_lib.identity(name, x.dtype) and np.array_equal(ex[1:], ref[:-1])
 
 
 def test_generate_input_matches_reference(golden, oracle_lib):
