@@ -1,22 +1,36 @@
-"""Small scans for compute-sanitizer (memcheck / racecheck / synccheck)."""
+"""Small scans for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
+
+    python scripts/sanitize_case.py [all|full|partial|generic|reduce]
+"""
 import os
 import sys
 
-import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1604_04815_b200 import scan as S  # noqa: E402
 
+mode = sys.argv[1] if len(sys.argv) > 1 else "all"
 for dt in (torch.int32, torch.float64):
-    for n in (5, 8192 * 3 + 7, 300_001):
-        x = (torch.arange(n, dtype=dt, device="cuda") % 7) - 3
-        y = S.inclusive_scan(x)
-        ref = torch.cumsum(x.double(), 0).to(dt)
-        assert torch.equal(y, ref), (dt, n)
-        S.exclusive_scan(x)
-        x2 = x[1:]  # misaligned -> generic kernel
-        S.inclusive_scan(x2)
-        S.reduce_sum(x)
+    tile = S.query_config(dt, 1 << 20)["tile_elems"]
+    sizes = {"full": (tile * 3, tile * 200), "partial": (5, tile * 3 + 7, 300_001),
+             "generic": (tile * 3 + 7,), "reduce": (300_001,)}
+    for m, ns in sizes.items():
+        if mode not in ("all", m):
+            continue
+        for n in ns:
+            x = (torch.arange(n + 1, dtype=dt, device="cuda") % 7) - 3
+            if m == "generic":
+                x = x[1:]  # misaligned -> generic kernel
+            else:
+                x = x[:n]
+            if m == "reduce":
+                S.reduce_sum(x)
+                continue
+            for op in ("add", "max"):
+                y = S.inclusive_scan(x, op=op)
+                ref = torch.cumsum(x.double(), 0).to(dt) if op == "add" else torch.cummax(x, 0).values
+                assert torch.equal(y, ref), (dt, n, m, op)
+                S.exclusive_scan(x, op=op)
 torch.cuda.synchronize()
-print("sanitize cases ok")
+print("sanitize cases ok", mode)
