@@ -68,6 +68,9 @@ ls_status cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
 
+// below this size a misaligned input stays on the generic kernel (one launch)
+constexpr int64_t kSplitMinElems = 1 << 20;
+
 bool valid_dtype(ls_dtype dt) { return dt >= LS_I32 && dt <= LS_F64; }
 bool valid_op(ls_op op) { return op >= LS_OP_ADD && op <= LS_OP_MIN; }
 
@@ -187,33 +190,14 @@ ls_status identity_fill(ls_op op, ls_dtype dt, void *dst, const void *carry_in, 
     return LS_OK;
 }
 
-ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, const void *carry_in, void *total_out,
-                    void *ws, size_t ws_bytes, void *stream, bool excl) {
-    if (!valid_dtype(dt)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported dtype code %d", (int)dt);
-    if (!valid_op(op)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported operator code %d", (int)op);
-    const int es = elem_size(dt);
-    if (n < 0) return fail(LS_ERR_INVALID_ARG, "n must be >= 0, got %lld", (long long)n);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (n > 0 && (!x || !y)) return fail(LS_ERR_INVALID_ARG, "x and y must be non-NULL for n > 0");
-    if (((uintptr_t)x % es) || ((uintptr_t)y % es))
-        return fail(LS_ERR_INVALID_ARG, "x and y must be aligned to the element size (%d)", es);
-    if (x != y && n > 0 && ranges_overlap(x, y, (size_t)n * es))
-        return fail(LS_ERR_INVALID_ARG, "x and y overlap without being identical (only exact in-place is allowed)");
-    if (total_out && carry_in && total_out == carry_in)
-        return fail(LS_ERR_INVALID_ARG, "total_out must not alias carry_in");
-    if (n == 0) return total_out ? identity_fill(op, dt, total_out, carry_in, s) : LS_OK;
-    ls_status st = check_ws_header(ws, ws_bytes, ls_workspace_bytes(dt, n));
-    if (st != LS_OK) return st;
-    DevState *d = nullptr;
-    if ((st = device_state(&d)) != LS_OK) return st;
-
-    const bool fast = (((uintptr_t)x | (uintptr_t)y) & 15u) == 0;
+// One kernel launch of the fast (TMA, 16-byte aligned) or generic path.
+ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
+                      const void *carry_in, void *total_out, void *ws, cudaStream_t s, bool excl, bool fast,
+                      const DebugCfg &dbg) {
     const Launch &L = K(dt).scan[op][excl][fast];
     const int64_t M = num_tiles(dt, n, fast);
-    const int64_t cap = (int64_t)d->occ[dt][op][excl][fast] * d->sms;
+    const int64_t cap = (int64_t)d.occ[dt][op][excl][fast] * d.sms;
     const int G = (int)std::min<int64_t>(M, cap);
-
-    const DebugCfg dbg = debug_snapshot();
     ScanParams p{};
     p.x = x;
     p.y = y;
@@ -246,6 +230,48 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
     cfg.numAttrs = 1;
     LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "scan kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    return LS_OK;
+}
+
+ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, const void *carry_in, void *total_out,
+                    void *ws, size_t ws_bytes, void *stream, bool excl) {
+    if (!valid_dtype(dt)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported dtype code %d", (int)dt);
+    if (!valid_op(op)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported operator code %d", (int)op);
+    const int es = elem_size(dt);
+    if (n < 0) return fail(LS_ERR_INVALID_ARG, "n must be >= 0, got %lld", (long long)n);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n > 0 && (!x || !y)) return fail(LS_ERR_INVALID_ARG, "x and y must be non-NULL for n > 0");
+    if (((uintptr_t)x % es) || ((uintptr_t)y % es))
+        return fail(LS_ERR_INVALID_ARG, "x and y must be aligned to the element size (%d)", es);
+    if (x != y && n > 0 && ranges_overlap(x, y, (size_t)n * es))
+        return fail(LS_ERR_INVALID_ARG, "x and y overlap without being identical (only exact in-place is allowed)");
+    if (total_out && carry_in && total_out == carry_in)
+        return fail(LS_ERR_INVALID_ARG, "total_out must not alias carry_in");
+    if (n == 0) return total_out ? identity_fill(op, dt, total_out, carry_in, s) : LS_OK;
+    ls_status st = check_ws_header(ws, ws_bytes, ls_workspace_bytes(dt, n));
+    if (st != LS_OK) return st;
+    DevState *d = nullptr;
+    if ((st = device_state(&d)) != LS_OK) return st;
+    const DebugCfg dbg = debug_snapshot();
+
+    const uintptr_t mx = (uintptr_t)x & 15u, my = (uintptr_t)y & 15u;
+    if (mx == 0 && my == 0) {
+        st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, true, dbg);
+    } else if (mx == my && n >= kSplitMinElems) {
+        // x and y share their misalignment (e.g. a slice scanned in place):
+        // the few head elements up to the 16-byte boundary go through the
+        // generic kernel, whose total carries into the TMA kernel for the rest
+        const int64_t head = (int64_t)((16u - mx) / (unsigned)es);
+        void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
+        st = launch_scan(*d, op, dt, x, y, head, carry_in, scratch, ws, s, excl, false, dbg);
+        if (st == LS_OK)
+            st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
+                             static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl, true,
+                             dbg);
+    } else {
+        st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, false, dbg);
+    }
+    if (st != LS_OK) return st;
     if (dbg.armed()) return read_device_error(ws, s, true);
     return LS_OK;
 }

@@ -20,6 +20,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lscan.h"
@@ -120,6 +121,28 @@ bool is_pinned(const void *p) {
 
 int esize(ls_dtype dt) { return (dt == LS_I32 || dt == LS_F32) ? 4 : 8; }
 
+// Host copy between pageable memory and the pinned staging buffers, split
+// over a few threads: a single core's memcpy (~5-10 GB/s) would otherwise
+// bound the pageable pipeline well below PCIe.
+void parallel_memcpy(void *dst, const void *src, size_t bytes) {
+    static const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned nt = std::max(1u, std::min(8u, hw ? hw : 1u));
+    if (bytes < ((size_t)4 << 20) || nt == 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t part = ((bytes / nt) + 4095) & ~(size_t)4095;
+    std::vector<std::thread> th;
+    for (unsigned i = 1; i < nt; ++i) {
+        const size_t off = part * i;
+        if (off >= bytes) break;
+        const size_t len = std::min(part, bytes - off);
+        th.emplace_back([=] { memcpy((char *)dst + off, (const char *)src + off, len); });
+    }
+    memcpy(dst, src, std::min(part, bytes));
+    for (auto &t : th) t.join();
+}
+
 }  // namespace
 
 extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
@@ -156,7 +179,7 @@ extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y,
         const int b = (int)(k % kBufs);
         const int64_t off = k * chunk, len = std::min(chunk, n - off);
         HC(cudaEventSynchronize(c->ev_out[b]), "copy-out wait");
-        memcpy(yb + off * es, c->pin_out[b], (size_t)len * es);
+        parallel_memcpy(yb + off * es, c->pin_out[b], (size_t)len * es);
         return LS_OK;
     };
 
@@ -172,7 +195,7 @@ extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y,
         const void *src = xb + off * es;
         if (!direct) {
             if (k >= kBufs) HC(cudaEventSynchronize(c->ev_in[b]), "staging reuse");
-            memcpy(c->pin_in[b], src, bytes);
+            parallel_memcpy(c->pin_in[b], src, bytes);
             src = c->pin_in[b];
         }
         HC(cudaMemcpyAsync(c->dbuf[b], src, bytes, cudaMemcpyHostToDevice, c->s_in), "copy-in");

@@ -143,6 +143,32 @@ def test_misaligned_generic_path(S, oracle_lib, tok):
 
 
 @pytest.mark.parametrize("tok", TOKS)
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_congruent_misalignment_split_path(S, oracle_lib, tok, shift):
+    # x and y misaligned by the same amount (a slice scanned in place, or two
+    # slices at equal offsets): head elements on the generic kernel, the rest
+    # on the TMA kernel with the head's total as carry
+    es = 4 if tok in ("i32", "f32") else 8
+    if (shift * es) % 16 == 0:
+        pytest.skip("aligned")
+    n = 3_000_011
+    x = oracle_lib.generate_input(n + shift, tok, [shift, n])
+    big = torch.from_numpy(x).cuda()
+    xd = big[shift:]
+    assert xd.data_ptr() % 16 != 0
+    tot = torch.empty(1, dtype=xd.dtype, device="cuda")
+    other = torch.empty(n + shift, dtype=xd.dtype, device="cuda")[shift:]
+    S.inclusive_scan(xd, out=other, total_out=tot)
+    check(x[shift:].copy(), other.cpu().numpy(), oracle_lib, what="split out-of-place")
+    S.exclusive_scan(xd, out=other)
+    check(x[shift:].copy(), other.cpu().numpy(), oracle_lib, exclusive=True, what="split exclusive")
+    S.inclusive_scan(xd, out=xd)
+    check(x[shift:].copy(), xd.cpu().numpy(), oracle_lib, what="split in-place")
+    if tok[0] == "i":
+        assert tot.item() == oracle_lib.c_sequential_scan(x[shift:].copy())[1]
+
+
+@pytest.mark.parametrize("tok", TOKS)
 def test_carry_in_total_out(S, oracle_lib, tok):
     n = 3_000_001
     x = oracle_lib.generate_input(n, tok, [1, 2])
