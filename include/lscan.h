@@ -96,6 +96,42 @@ ls_status ls_reduce_sum(ls_dtype dt, const void *x, int64_t n, void *total_out,
 ls_status ls_carry_from_totals(ls_op op, ls_dtype dt, const void *totals, int64_t count,
                                int64_t rank, void *carry_out, void *stream);
 
+/* ---- multi-GPU, block-cyclic (fused exchange) --------------------
+ * `world` GPUs (one process each) scan one global array distributed
+ * block-cyclically, the reference's cyclic block ownership (chained.py:264-287)
+ * lifted from workers to GPUs: every GPU holds n_local elements (the same n_local
+ * on every GPU) cut into stripes of G tiles (G = the launch grid, identical on
+ * every GPU), and the global order is stripe 0 of GPU 0, stripe 0 of GPU 1, ...,
+ * stripe 1 of GPU 0, ...  One kernel per GPU does everything: stripe aggregates
+ * are pushed into every GPU's exchange region (peer memory over NVLink,
+ * system-scope tagged words) as soon as the data lands, and one warp per GPU
+ * folds them into the global round chain — no host synchronisation, no NCCL.
+ * xchg: this GPU's exchange region (ls_xchg_bytes, zeroed once with
+ *   ls_workspace_init before ANY GPU's first call — barrier after init);
+ * xchg_peers: device array of `world` pointers, entry g = GPU g's exchange
+ *   region as mapped in this process (entry rank = xchg);
+ * grid > 0 caps the CTAs (equal on every GPU), 0 = the device's capacity.
+ * total_out receives the GLOBAL total.  All GPUs must make the same sequence
+ * of calls.  The debug watchdog applies, but these calls never synchronise on
+ * it (all GPUs of a call must be in flight together): read the outcome with
+ * ls_workspace_error. */
+size_t ls_xchg_bytes(ls_dtype dt, int world, int64_t n_local);
+ls_status ls_inclusive_scan_multi(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n_local,
+                                  const void *carry_in, void *total_out, void *ws, size_t ws_bytes,
+                                  int rank, int world, void *xchg, size_t xchg_bytes,
+                                  void *const *xchg_peers, int grid, void *stream);
+ls_status ls_exclusive_scan_multi(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n_local,
+                                  const void *carry_in, void *total_out, void *ws, size_t ws_bytes,
+                                  int rank, int world, void *xchg, size_t xchg_bytes,
+                                  void *const *xchg_peers, int grid, void *stream);
+/* Device memory that can be shared with peer processes (cudaMalloc'd), and
+ * CUDA IPC handles (64 bytes) to map it in another process. */
+ls_status ls_device_alloc(size_t bytes, void **out);
+ls_status ls_device_free(void *ptr);
+ls_status ls_ipc_get_handle(void *dev_ptr, void *handle_out);
+ls_status ls_ipc_open(const void *handle, void **dev_ptr_out);
+ls_status ls_ipc_close(void *dev_ptr);
+
 /* ---- host-buffer entry (what chained_scan(problem) does with numpy arrays) --
  * x and y are HOST pointers (pinned or pageable; y may equal x).  The array
  * is streamed through the device in chunks with copy-in, scan and copy-out

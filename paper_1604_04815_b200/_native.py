@@ -47,7 +47,8 @@ EXPORTED = [
     "ls_exclusive_sum", "ls_reduce", "ls_reduce_sum", "ls_carry_from_totals", "ls_scan_host",
     "ls_inclusive_sum_host", "ls_debug_config", "ls_debug_perturb",
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
-    "ls_query_config", "ls_launch_count",
+    "ls_query_config", "ls_launch_count", "ls_xchg_bytes", "ls_inclusive_scan_multi", "ls_exclusive_scan_multi",
+    "ls_device_alloc", "ls_device_free", "ls_ipc_get_handle", "ls_ipc_open", "ls_ipc_close",
 ]
 
 
@@ -130,6 +131,14 @@ def lib():
             "ls_abi_version": (ci, []),
             "ls_query_config": (ci, [ci, i64, ctypes.POINTER(ctypes.c_int64)]),
             "ls_launch_count": (i64, []),
+            "ls_xchg_bytes": (sz, [ci, ci, i64]),
+            "ls_inclusive_scan_multi": (ci, [ci, ci, vp, vp, i64, vp, vp, vp, sz, ci, ci, vp, sz, vp, ci, vp]),
+            "ls_exclusive_scan_multi": (ci, [ci, ci, vp, vp, i64, vp, vp, vp, sz, ci, ci, vp, sz, vp, ci, vp]),
+            "ls_device_alloc": (ci, [sz, ctypes.POINTER(ctypes.c_void_p)]),
+            "ls_device_free": (ci, [vp]),
+            "ls_ipc_get_handle": (ci, [vp, vp]),
+            "ls_ipc_open": (ci, [vp, ctypes.POINTER(ctypes.c_void_p)]),
+            "ls_ipc_close": (ci, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -105,6 +105,7 @@ struct DevState {
     bool init = false;
     int sms = 0;
     int occ[4][kNumOps][2][2] = {};  // resident CTAs per SM [dtype][op][excl][fast]
+    int occ_multi[4][kNumOps][2] = {};
     int reduce_occ[4][kNumOps] = {};
 };
 std::mutex g_dev_mu;
@@ -134,6 +135,17 @@ ls_status device_state(DevState **out) {
                         if (occ < 1) return fail(LS_ERR_CUDA, "scan kernel cannot be resident (smem %zu B)", L.smem);
                         d.occ[dt][op][ex][fa] = occ;
                     }
+                for (int ex = 0; ex < 2; ++ex) {
+                    const Launch &L = k.multi[op][ex];
+                    LS_CUDA(cudaFuncSetAttribute((const void *)L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)L.smem),
+                            "cudaFuncSetAttribute(max dynamic smem)");
+                    int occm = 0;
+                    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occm, (const void *)L.fn, L.threads, L.smem),
+                            "occupancy query");
+                    if (occm < 1) return fail(LS_ERR_CUDA, "multi scan kernel cannot be resident");
+                    d.occ_multi[dt][op][ex] = occm;
+                }
                 int occ = 0;
                 LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.reduce_fn[op], kReduceThreads, 0),
                         "occupancy");
@@ -309,7 +321,7 @@ size_t ls_workspace_bytes(ls_dtype dt, int64_t n) {
 }
 
 ls_status ls_workspace_init(void *ws, size_t ws_bytes, void *stream) {
-    if (!ws || ws_bytes < kSlotBase) return fail(LS_ERR_WORKSPACE, "workspace NULL or smaller than its header");
+    if (!ws || ws_bytes < sizeof(Header)) return fail(LS_ERR_WORKSPACE, "workspace NULL or smaller than its header");
     LS_CUDA(cudaMemsetAsync(ws, 0, ws_bytes, static_cast<cudaStream_t>(stream)), "workspace memset");
     return LS_OK;
 }
@@ -371,6 +383,126 @@ ls_status ls_carry_from_totals(ls_op op, ls_dtype dt, const void *totals, int64_
     K(dt).launch_carry(op, totals, rank, carry_out, static_cast<cudaStream_t>(stream));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LS_CUDA(cudaGetLastError(), "carry kernel launch");
+    return LS_OK;
+}
+
+size_t ls_xchg_bytes(ls_dtype dt, int world, int64_t n_local) {
+    if (!valid_dtype(dt) || world < 1 || n_local < 0) return 0;
+    const int64_t rounds = std::max<int64_t>(num_tiles(dt, n_local, true), 1);  // rounds <= tiles
+    const size_t sw = elem_size(dt) == 4 ? 8 : 16;
+    const size_t bytes = kXchgSlotBase + 2 * (size_t)rounds * (size_t)world * sw;
+    return (bytes + 255) & ~(size_t)255;
+}
+
+static ls_status scan_multi_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, const void *carry_in,
+                                 void *total_out, void *ws, size_t ws_bytes, int rank, int world, void *xchg,
+                                 size_t xchg_bytes, void *const *peers, int grid, void *stream, bool excl) {
+    if (!valid_dtype(dt)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported dtype code %d", (int)dt);
+    if (!valid_op(op)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported operator code %d", (int)op);
+    if (world < 1 || world > 32 || rank < 0 || rank >= world) return fail(LS_ERR_INVALID_ARG, "bad rank/world");
+    if (n < 1 || !x || !y) return fail(LS_ERR_INVALID_ARG, "multi-GPU scan needs n >= 1 and device buffers");
+    if ((((uintptr_t)x | (uintptr_t)y) & 15u) != 0)
+        return fail(LS_ERR_INVALID_ARG, "multi-GPU scan needs 16-byte aligned x and y");
+    const int es = elem_size(dt);
+    if (x != y && ranges_overlap(x, y, (size_t)n * es))
+        return fail(LS_ERR_INVALID_ARG, "x and y overlap without being identical");
+    if (!xchg || !peers || xchg_bytes < ls_xchg_bytes(dt, world, n) || ((uintptr_t)xchg & 127u))
+        return fail(LS_ERR_WORKSPACE, "exchange region missing, misaligned or too small");
+    ls_status st = check_ws_header(ws, ws_bytes, ls_workspace_bytes(dt, n));
+    if (st != LS_OK) return st;
+    DevState *d = nullptr;
+    if ((st = device_state(&d)) != LS_OK) return st;
+    const Launch &L = K(dt).multi[op][excl];
+    const int64_t M = num_tiles(dt, n, true);
+    const int64_t cap = (int64_t)d->occ_multi[dt][op][excl] * d->sms;
+    int64_t G = std::min<int64_t>(M, cap);
+    if (grid > 0) {
+        if (grid > cap) return fail(LS_ERR_INVALID_ARG, "grid %d exceeds co-resident capacity %lld", grid, (long long)cap);
+        G = std::min<int64_t>(M, grid);
+    }
+    const DebugCfg dbg = debug_snapshot();
+    ScanParams p{};
+    p.x = x;
+    p.y = y;
+    p.n = n;
+    p.carry_in = carry_in;
+    p.total_out = total_out;
+    p.ws = static_cast<uint8_t *>(ws);
+    p.num_tiles = M;
+    p.spin_budget = dbg.spin_budget;
+    p.corrupt_tile = dbg.corrupt;
+    p.protocol_checks = dbg.protocol;
+    p.delay_red_ns = dbg.delay_red_ns;
+    p.delay_scan_ns = dbg.delay_scan_ns;
+    p.stall_tile = dbg.spin_budget > 0 ? dbg.stall_tile : -1;
+    p.rank = rank;
+    p.world = world;
+    p.xchg = static_cast<uint8_t *>(xchg);
+    p.xchg_peers = reinterpret_cast<uint64_t *const *>(peers);
+    p.xchg_rounds = std::max<int64_t>(M, 1);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3((unsigned)L.threads);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "multi scan kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    // no debug synchronisation here: the GPUs of one call must all be in
+    // flight together; read the error word afterwards (ls_workspace_error)
+    return LS_OK;
+}
+
+ls_status ls_inclusive_scan_multi(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n_local,
+                                  const void *carry_in, void *total_out, void *ws, size_t ws_bytes, int rank,
+                                  int world, void *xchg, size_t xchg_bytes, void *const *xchg_peers, int grid,
+                                  void *stream) {
+    return scan_multi_impl(op, dt, x, y, n_local, carry_in, total_out, ws, ws_bytes, rank, world, xchg, xchg_bytes,
+                           xchg_peers, grid, stream, false);
+}
+
+ls_status ls_exclusive_scan_multi(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n_local,
+                                  const void *carry_in, void *total_out, void *ws, size_t ws_bytes, int rank,
+                                  int world, void *xchg, size_t xchg_bytes, void *const *xchg_peers, int grid,
+                                  void *stream) {
+    return scan_multi_impl(op, dt, x, y, n_local, carry_in, total_out, ws, ws_bytes, rank, world, xchg, xchg_bytes,
+                           xchg_peers, grid, stream, true);
+}
+
+ls_status ls_device_alloc(size_t bytes, void **out) {
+    if (!out) return fail(LS_ERR_INVALID_ARG, "out is NULL");
+    LS_CUDA(cudaMalloc(out, bytes), "cudaMalloc");
+    return LS_OK;
+}
+
+ls_status ls_device_free(void *ptr) {
+    LS_CUDA(cudaFree(ptr), "cudaFree");
+    return LS_OK;
+}
+
+ls_status ls_ipc_get_handle(void *dev_ptr, void *handle_out) {
+    if (!dev_ptr || !handle_out) return fail(LS_ERR_INVALID_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    LS_CUDA(cudaIpcGetMemHandle(&h, dev_ptr), "cudaIpcGetMemHandle");
+    memcpy(handle_out, &h, sizeof h);
+    return LS_OK;
+}
+
+ls_status ls_ipc_open(const void *handle, void **dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return fail(LS_ERR_INVALID_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    LS_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return LS_OK;
+}
+
+ls_status ls_ipc_close(void *dev_ptr) {
+    LS_CUDA(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
     return LS_OK;
 }
 

@@ -133,7 +133,15 @@ struct ScanParams {
     int64_t delay_red_ns;   // debug: reducer sleeps this long on tiles t % 3 == 1 (timing perturbation)
     int64_t delay_scan_ns;  // debug: scanners sleep this long on tiles t % 3 == 2
     int64_t stall_tile;     // debug: this tile never publishes its aggregate (needs a spin budget)
+    // ---- multi-GPU (block-cyclic stripes, scan_ws2_kernel<..., MULTI=true>) ----
+    int rank, world;               // this GPU's place among `world` GPUs
+    uint8_t *xchg;                 // this GPU's exchange region (header + 2 parities of slots)
+    uint64_t *const *xchg_peers;   // device array: every GPU's exchange slot base (index = rank)
+    int64_t xchg_rounds;           // round capacity per parity
 };
+
+// cross-GPU exchange region: [Header][parity 0: rounds x world slots][parity 1: ...]
+constexpr size_t kXchgSlotBase = 128;
 
 __device__ __forceinline__ void debug_sleep(int64_t ns) {
     while (ns > 0) {
@@ -169,6 +177,18 @@ struct Slot {
         const uint64_t *p = arr + idx * W;
 #pragma unroll
         for (int i = 0; i < W; ++i) w[i] = slot_ld(p + i);
+    }
+    // system-scope variants for slots written by other GPUs
+    __device__ static void publish_sys(uint64_t *arr, int64_t idx, uint32_t tag, T v) {
+        uint64_t *p = arr + idx * W;
+        const uint64_t b = (uint64_t)Elem<T>::bits(v);
+        slot_st_sys(p, ((uint64_t)tag << 32) | (b & 0xffffffffull));
+        if constexpr (W == 2) slot_st_sys(p + 1, ((uint64_t)tag << 32) | (b >> 32));
+    }
+    __device__ static void load_sys(const uint64_t *arr, int64_t idx, uint64_t (&w)[W]) {
+        const uint64_t *p = arr + idx * W;
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[i] = slot_ld_sys(p + i);
     }
 };
 

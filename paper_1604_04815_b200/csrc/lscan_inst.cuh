@@ -15,6 +15,14 @@ Launch fast_launch() {
 }
 
 template <typename T, typename OP, bool EXCL>
+Launch multi_launch() {
+    using C = FastCfg<sizeof(T)>;
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true>,
+            ws2_threads<C::kScanWarps, true>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(),
+            C::kTileBytes, C::kStages};
+}
+
+template <typename T, typename OP, bool EXCL>
 Launch generic_launch() {
     return {&scan_generic_kernel<T, OP, kGenThreads, kGenTileBytes, EXCL>, kGenThreads,
             scan_generic_smem_bytes<T, kGenThreads, kGenTileBytes>(), kGenTileBytes, 1};
@@ -26,6 +34,8 @@ void fill_op(DtypeKernels &k) {
     k.scan[OP::code][1][1] = fast_launch<T, OP, true>();
     k.scan[OP::code][0][0] = generic_launch<T, OP, false>();
     k.scan[OP::code][1][0] = generic_launch<T, OP, true>();
+    k.multi[OP::code][0] = multi_launch<T, OP, false>();
+    k.multi[OP::code][1] = multi_launch<T, OP, true>();
     k.reduce_fn[OP::code] = (const void *)&reduce_kernel<T, OP, kReduceThreads>;
 }
 

@@ -73,8 +73,8 @@ struct LookbackOut {
 // carries `tag`; a spin budget turns a stall into LS_ERR_LIVENESS.
 template <typename T, typename OP>
 __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, const uint64_t *rnd, int64_t k, int c,
-                                                       int G, bool need_r, bool want_own, uint32_t tag, int lane,
-                                                       int64_t spin_budget, Header *hdr, uint32_t where) {
+                                                       int G, bool need_r, int64_t r_idx, bool want_own, uint32_t tag,
+                                                       int lane, int64_t spin_budget, Header *hdr, uint32_t where) {
     using S = Slot<T>;
     constexpr int U = 5;  // 160 slots per pass covers a 148-SM round
     const T ident = OP::template identity<T>();
@@ -84,7 +84,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
     int64_t probes = 0;
     bool r_pending = need_r;
     uint64_t rw[S::W];
-    if (need_r) S::load(rnd, k - 1, rw);
+    if (need_r) S::load(rnd, r_idx, rw);
     for (int base = 0; base < count || r_pending; base += 32 * U) {
         uint64_t w[U][S::W];
         bool need[U];
@@ -118,7 +118,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
                 break;
             }
             __nanosleep(32);
-            if (r_pending) S::load(rnd, k - 1, rw);
+            if (r_pending) S::load(rnd, r_idx, rw);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int j = base + u * 32 + lane;
@@ -139,16 +139,29 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
     return o;
 }
 
-template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL>
-__global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(const ScanParams p) {
+template <int SCAN_WARPS, bool MULTI>
+__host__ __device__ constexpr int ws2_threads() { return (SCAN_WARPS + (MULTI ? 5 : 3)) * 32; }
+
+// Cross-GPU round chain helpers (MULTI): the exchange slot of (round k, gpu g)
+// in a GPU's exchange region, double-buffered by call parity so a fast GPU's
+// next call can never overwrite a slot a slow GPU still reads.
+template <typename T>
+__device__ __forceinline__ uint64_t *xchg_slots(uint8_t *region, uint32_t xtag, int64_t rounds_cap, int world) {
+    return reinterpret_cast<uint64_t *>(region + kXchgSlotBase) +
+           (int64_t)(xtag & 1u) * rounds_cap * world * Slot<T>::W;
+}
+
+template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL, bool MULTI = false>
+__global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_kernel(const ScanParams p) {
     constexpr int SCAN_THREADS = SCAN_WARPS * 32;
     constexpr int V = TILE_BYTES / SCAN_THREADS / 16;  // rows (16-byte vectors) per lane
     constexpr int PER = 16 / (int)sizeof(T);           // elements per vector
     constexpr int TILE_ELEMS = TILE_BYTES / (int)sizeof(T);
     constexpr int WARP_BYTES = TILE_BYTES / SCAN_WARPS;
     constexpr int W_PROD = SCAN_WARPS, W_RED = SCAN_WARPS + 1, W_AUX = SCAN_WARPS + 2;
+    constexpr int W_PUSH = SCAN_WARPS + 3, W_GCHAIN = SCAN_WARPS + 4;  // MULTI only, CTA G-1 only
     static_assert(V >= 1 && TILE_BYTES % (SCAN_THREADS * 16) == 0, "whole rows per lane");
-    static_assert(SCAN_WARPS >= 2 && SCAN_WARPS + 3 <= 32, "2..29 scanner warps");
+    static_assert(SCAN_WARPS >= 2 && ws2_threads<SCAN_WARPS, MULTI>() <= 1024, "too many warps");
     using S = Slot<T>;
     const T ident = OP::template identity<T>();
 
@@ -174,6 +187,8 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
     const uint32_t tag = call_tag(hdr);
     const int64_t my_tiles = (M - c + G - 1) / G;
     const int64_t full_tiles = p.n / TILE_ELEMS;
+    Header *xhdr = MULTI ? reinterpret_cast<Header *>(p.xchg) : nullptr;
+    const uint32_t xtag = MULTI ? call_tag(xhdr) : 0u;
 
     if (tid == 0) {
 #pragma unroll
@@ -263,25 +278,39 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
         for (int64_t k = 0; k < my_tiles; ++k) {
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
-            const bool chain = (c == G - 1) && (t + 1 < M);
-            // R[k-1]: the caller's carry in round 0, the chain owner's register,
-            // or the published round slot for everyone else
-            const bool need_r = k > 0 && c != G - 1;
-            const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, chain, tag, lane,
-                                                          p.spin_budget, hdr, (uint32_t)t);
             bool has;
-            T base;
-            if (k == 0) { has = have_carry; base = r_prev; }
-            else if (c == G - 1) { has = true; base = r_prev; }
-            else { has = true; base = lb.r; }
-            T prefix = base;
-            if (c > 0) {
-                prefix = has ? OP::apply(base, lb.sum) : lb.sum;
-                has = true;
-            }
-            if (chain) {
-                r_prev = has ? OP::apply(prefix, lb.own) : lb.own;  // R[k]
-                if (lane == 0) S::publish(rnd, k, tag, r_prev);
+            T prefix;
+            if constexpr (MULTI) {
+                // X[k] = everything before this GPU's k-th stripe, published by
+                // the global-chain warp of CTA G-1
+                const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, k, c, G, true, k, false, tag, lane,
+                                                              p.spin_budget, hdr, (uint32_t)t);
+                has = k > 0 || p.rank > 0 || have_carry;
+                prefix = lb.r;
+                if (c > 0) {
+                    prefix = has ? OP::apply(lb.r, lb.sum) : lb.sum;
+                    has = true;
+                }
+            } else {
+                const bool chain = (c == G - 1) && (t + 1 < M);
+                // R[k-1]: the caller's carry in round 0, the chain owner's register,
+                // or the published round slot for everyone else
+                const bool need_r = k > 0 && c != G - 1;
+                const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, k - 1, chain, tag, lane,
+                                                              p.spin_budget, hdr, (uint32_t)t);
+                T base;
+                if (k == 0) { has = have_carry; base = r_prev; }
+                else if (c == G - 1) { has = true; base = r_prev; }
+                else { has = true; base = lb.r; }
+                prefix = base;
+                if (c > 0) {
+                    prefix = has ? OP::apply(base, lb.sum) : lb.sum;
+                    has = true;
+                }
+                if (chain) {
+                    r_prev = has ? OP::apply(prefix, lb.own) : lb.own;  // R[k]
+                    if (lane == 0) S::publish(rnd, k, tag, r_prev);
+                }
             }
             if (k >= STAGES) mbar_wait(&pre_free[s], (uint32_t)(((k - STAGES) / STAGES) & 1));
             if (lane == 0) {
@@ -291,7 +320,67 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
             }
             __syncwarp();
         }
-    } else {
+    } else if (MULTI && warp == W_PUSH) {
+        // ------------------------------------------- stripe aggregate pusher
+        // (CTA G-1 only) BA[k] = A[kG] (+) ... (+) A[kG+G-1], stored into every
+        // GPU's exchange slot (k, rank) as soon as this GPU's round k landed
+        if (c == G - 1) {
+            const int64_t rounds = (M + G - 1) / G;
+            uint64_t *peer = lane < p.world ? p.xchg_peers[lane] : nullptr;
+            for (int64_t k = 0; k < rounds; ++k) {
+                const int cnt = (int)((M - k * G) < G ? (M - k * G) : G);
+                const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, k, cnt, G, false, 0, false, tag, lane,
+                                                              p.spin_budget, hdr, (uint32_t)(k * G));
+                if (lane < p.world) {
+                    uint64_t *slots = xchg_slots<T>(reinterpret_cast<uint8_t *>(peer), xtag, p.xchg_rounds, p.world);
+                    S::publish_sys(slots, k * p.world + p.rank, xtag, lb.sum);
+                }
+            }
+        }
+    } else if (MULTI && warp == W_GCHAIN) {
+        // -------------------------------------------------- global chain
+        // (CTA G-1 only) X[k] = GB[k-1] (+) BA[k][0] (+) ... (+) BA[k][rank-1];
+        // GB[k] = X[k] (+) BA[k][rank] (+) ... (+) BA[k][world-1]; every GPU
+        // folds the same values in the same order, so all agree bit for bit
+        if (c == G - 1) {
+            const T *carry_in = static_cast<const T *>(p.carry_in);
+            bool have_gb = carry_in != nullptr;
+            T gb = have_gb ? *carry_in : ident;
+            const int64_t rounds = (M + G - 1) / G;
+            uint64_t *slots = xchg_slots<T>(p.xchg, xtag, p.xchg_rounds, p.world);
+            int64_t probes = 0;
+            for (int64_t k = 0; k < rounds; ++k) {
+                T v = ident;
+                uint64_t w[S::W];
+                bool ok = lane >= p.world;
+                if (!ok) S::load_sys(slots, k * p.world + lane, w);
+                while (true) {
+                    if (!ok) ok = S::decode(w, xtag, v);
+                    if (__all_sync(0xffffffffu, ok)) break;
+                    if (p.spin_budget > 0 && ++probes > p.spin_budget) {
+                        if (lane == 0) raise_error(hdr, 4u /*LS_ERR_LIVENESS*/, (uint32_t)(k * G));
+                        if (!ok) { v = ident; ok = true; }
+                        break;
+                    }
+                    __nanosleep(32);
+                    if (!ok) S::load_sys(slots, k * p.world + lane, w);
+                }
+                T x = gb;  // fold in GPU order; lane-uniform
+                bool hx = have_gb;
+                for (int g = 0; g < p.world; ++g) {
+                    const T bg = __shfl_sync(0xffffffffu, v, g);
+                    if (g == p.rank) {
+                        if (lane == 0) S::publish(rnd, k, tag, x);  // X[k]
+                    }
+                    x = hx ? OP::apply(x, bg) : bg;
+                    hx = true;
+                }
+                gb = x;
+                have_gb = true;
+            }
+            if (p.total_out != nullptr && lane == 0) *static_cast<T *>(p.total_out) = gb;
+        }
+    } else if (warp < SCAN_WARPS) {
         // ------------------------------------------------------------ scanners
         const uint32_t wbase = (uint32_t)warp * WARP_BYTES + (uint32_t)lane * 16;  // row 0 of this lane
         for (int64_t k = 0; k < my_tiles; ++k) {
@@ -336,7 +425,7 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
                 const T wi = warp_inclusive_scan<T, OP>(wt, lane);
                 const T we = __shfl_up_sync(0xffffffffu, wi, 1);
                 if (lane < SCAN_WARPS) warp_exc[lane] = we;
-                if (t == M - 1 && p.total_out != nullptr) {
+                if (!MULTI && t == M - 1 && p.total_out != nullptr) {
                     mbar_wait(&pre_ready[s], parity);
                     const T blk = __shfl_sync(0xffffffffu, wi, SCAN_WARPS - 1);
                     if (lane == 0) *static_cast<T *>(p.total_out) = pre_has[s] ? OP::apply(pre[s], blk) : blk;
@@ -383,7 +472,20 @@ __global__ void __launch_bounds__((SCAN_WARPS + 3) * 32, 1) scan_ws2_kernel(cons
     }
 
     __syncthreads();
-    if (tid == 0) epoch_handover(hdr, tag, G);
+    if (tid == 0) {
+        if constexpr (MULTI) {
+            // the exchange epoch advances with the workspace epoch: the last
+            // CTA of this GPU records both
+            const uint32_t old = atom_add_acqrel_u32(&hdr->done, 1u);
+            if (old == (uint32_t)G - 1u) {
+                st_relaxed_u32(&hdr->done, 0u);
+                st_relaxed_u32(&xhdr->epoch, xtag);
+                st_relaxed_u32(&hdr->epoch, tag);
+            }
+        } else {
+            epoch_handover(hdr, tag, G);
+        }
+    }
 }
 
 template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES>

@@ -81,3 +81,146 @@ def sharded_scan(shard: torch.Tensor, *, exclusive: bool = False, group=None,
     if res is not out:
         out.copy_(res)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Block-cyclic multi-GPU scan with the exchange fused into the scan kernel.
+
+def cyclic_layout(n_local: int, world: int, stripe: int):
+    """Global index of every local element for the block-cyclic layout:
+    stripe k of GPU g holds global elements [(k*world + g)*stripe, ... + stripe).
+    Returns a function local_index -> global_index (for tests and loaders); all
+    GPUs hold the same n_local, the last stripe of each GPU may be short."""
+    import numpy as np
+
+    def to_global(rank: int, j):
+        j = np.asarray(j)
+        k, r = np.divmod(j, stripe)
+        full_rounds = n_local // stripe
+        short = n_local - full_rounds * stripe
+        # rounds before the (possibly short) last one are full on every GPU
+        base = np.where(k < full_rounds, (k * world + rank) * stripe,
+                        full_rounds * world * stripe + rank * short)
+        return base + r
+
+    return to_global
+
+
+class CyclicScan:
+    """One process per GPU; every GPU scans its block-cyclic share of one
+    global array in a single kernel launch, exchanging stripe aggregates with
+    its peers through NVLink peer memory (include/lscan.h
+    ``ls_inclusive_scan_multi``).  Construct collectively; call collectively.
+
+    ``stripe_elems`` (= grid x tile elements) fixes the layout: GPU g's local
+    stripe k is global block ``k*world + g`` (see ``cyclic_layout``)."""
+
+    def __init__(self, dtype: torch.dtype, n_local: int, group=None, grid: int = 0):
+        import ctypes
+
+        from . import _native as N
+        from . import scan as S
+        from .errors import raise_for_status
+        self._N, self._S, self._raise = N, S, raise_for_status
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.dtype = dtype
+        self.dt = S.dtype_code(dtype)
+        self.n_local = int(n_local)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        L = N.lib()
+        cfg = S.query_config(dtype, self.n_local)
+        self.grid = int(grid) if grid > 0 else int(cfg["grid"])
+        self.stripe_elems = self.grid * int(cfg["tile_elems"])
+        meta = [None] * self.world
+        dist.all_gather_object(meta, (self.n_local, self.grid, str(dtype)), group=group)
+        if any(m != meta[0] for m in meta):
+            raise ValueError(f"every GPU must use the same n_local, grid and dtype: {meta}")
+        self.xbytes = int(L.ls_xchg_bytes(self.dt, self.world, self.n_local))
+        ptr = ctypes.c_void_p()
+        raise_for_status(L.ls_device_alloc(self.xbytes, ctypes.byref(ptr)))
+        self.xchg = ptr.value
+        raise_for_status(L.ls_workspace_init(self.xchg, self.xbytes, None))
+        torch.cuda.synchronize()
+        handle = ctypes.create_string_buffer(64)
+        raise_for_status(L.ls_ipc_get_handle(self.xchg, handle))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self._opened = []
+        peers = []
+        for g, h in enumerate(handles):
+            if g == self.rank:
+                peers.append(self.xchg)
+                continue
+            p = ctypes.c_void_p()
+            raise_for_status(L.ls_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
+            self._opened.append(p.value)
+            peers.append(p.value)
+        self.peers = torch.tensor(peers, dtype=torch.int64, device=self.device)
+        # nobody may push into a peer's region before that peer zeroed it
+        dist.barrier(group=group)
+
+    def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, *, op: str = "add",
+                 exclusive: bool = False, carry_in: Optional[torch.Tensor] = None,
+                 total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        S, N = self._S, self._N
+        if x.numel() != self.n_local or x.dtype != self.dtype or not x.is_contiguous():
+            raise ValueError("x must be the contiguous local share this scanner was built for")
+        if out is None:
+            out = torch.empty_like(x)
+        stream = torch.cuda.current_stream(x.device)
+        L = N.lib()
+        ws = S.workspace(x.device, stream, L.ls_workspace_bytes(self.dt, self.n_local))
+        fn = L.ls_exclusive_scan_multi if exclusive else L.ls_inclusive_scan_multi
+        rc = fn(S.op_code(op), self.dt, x.data_ptr(), out.data_ptr(), self.n_local,
+                None if carry_in is None else carry_in.data_ptr(),
+                None if total_out is None else total_out.data_ptr(), ws.data_ptr(), ws.numel(),
+                self.rank, self.world, self.xchg, self.xbytes, self.peers.data_ptr(), self.grid,
+                stream.cuda_stream)
+        self._raise(rc)
+        return out
+
+    def close(self):
+        L = self._N.lib()
+        torch.cuda.synchronize()
+        for p in self._opened:
+            L.ls_ipc_close(p)
+        self._opened = []
+        if self.xchg:
+            L.ls_device_free(self.xchg)
+            self.xchg = None
+
+
+def check_cyclic(scanner: "CyclicScan", x: torch.Tensor, y: torch.Tensor) -> bool:
+    """Independent exact check of a block-cyclic integer add scan, with no
+    scan of the data: within every stripe y[j] - y[j-1] == x[j] (wrapping),
+    and the first element of stripe (k, g) equals the wrapped sum of every
+    earlier stripe of every GPU (stripe sums all-gathered, tiny) plus x.
+    Integer dtypes only."""
+    if x.dtype.is_floating_point:
+        raise ValueError("check_cyclic is exact and needs an integer dtype")
+    n, S = x.numel(), scanner.stripe_elems
+    starts = torch.arange(0, n, S, device=x.device)
+    d = torch.empty_like(y)
+    d[1:] = y[1:] - y[:-1]
+    d[starts] = x[starts]  # stripe heads are checked against the global prefix below
+    ok = bool(torch.equal(d, x))
+    # stripe sums (wrapping, in the element type) of this GPU, then everyone's
+    full = n // S
+    parts = [x[:full * S].view(full, S).sum(1, dtype=torch.int64)]
+    if n % S:
+        parts.append(x[full * S:].sum(dtype=torch.int64).reshape(1))
+    sums = torch.cat(parts).to(x.dtype)
+    allsums = torch.empty(scanner.world, sums.numel(), dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(allsums, sums.contiguous(), group=scanner.group) \
+        if dist.get_backend(scanner.group) == "nccl" else \
+        dist.all_gather(list(allsums.unbind(0)), sums, group=scanner.group)
+    order = allsums.t().reshape(-1)  # global stripe order: round-major, then GPU
+    excl = torch.cumsum(order.to(torch.int64), 0) - order.to(torch.int64)
+    mine = excl.reshape(-1, scanner.world)[:, scanner.rank].to(x.dtype)  # wraps back to the element type
+    heads = (mine + x[starts]).to(x.dtype)
+    ok = ok and bool(torch.equal(y[starts], heads))
+    flag = torch.tensor([1 if ok else 0], device=x.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=scanner.group)
+    return bool(flag.item())
