@@ -63,3 +63,38 @@ def test_nccl_world_one(S, oracle_lib):
         assert np.array_equal(out.cpu().numpy(), oracle_lib.c_sequential_scan(x, exclusive=True)[0])
     finally:
         dist.destroy_process_group()
+
+
+def test_cyclic_scan_world_one(S, oracle_lib):
+    # the fused block-cyclic scanner end to end through torch.distributed
+    # (NCCL, world size 1): IPC export of the exchange region, the kernel,
+    # and the exact independent check
+    import torch.distributed as dist
+
+    from paper_1604_04815_b200.distributed import CyclicScan, check_cyclic
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 4_000_037
+        for tok, tdt in (("i32", torch.int32), ("i64", torch.int64)):
+            x = oracle_lib.generate_input(n, tok, [2, 2])
+            xd = torch.from_numpy(x).cuda()
+            sc = CyclicScan(tdt, n)
+            try:
+                tot = torch.empty(1, dtype=tdt, device="cuda")
+                y = sc(xd, total_out=tot)
+                ref = oracle_lib.c_sequential_scan(x)
+                assert np.array_equal(y.cpu().numpy(), ref[0]) and tot.item() == ref[1]
+                assert check_cyclic(sc, xd, y)
+                y[12345] += 1
+                assert not check_cyclic(sc, xd, y)
+                ye = sc(xd, exclusive=True, op="max")
+                assert np.array_equal(ye.cpu().numpy(), oracle_lib.exclusive_scan(x, "max"))
+            finally:
+                sc.close()
+    finally:
+        dist.destroy_process_group()
