@@ -441,6 +441,15 @@ def run_ours(args):
             del x2, y2
             torch.cuda.empty_cache()
         out["per_dtype"] = per
+        # the other modes of the same kernel on the headline array
+        modes = {}
+        for name, fn in (("exclusive_add", lambda: S.exclusive_scan(xd, yd)),
+                         ("inclusive_max", lambda: S.inclusive_scan(xd, yd, op="max")),
+                         ("inclusive_min", lambda: S.inclusive_scan(xd, yd, op="min")),
+                         ("in_place_add", lambda: S.inclusive_scan(yd, yd))):
+            msm = time_device(fn, 30, 3, stream)
+            modes[f"{tok}_{name}"] = round(n / (msm * 1e-3) * 1e-9, 2)
+        out["modes_gelems"] = modes
 
     if not args.no_cpu and rank == 0 and not use_dist:
         out["cpu_baseline"] = cpu_reference(tok, n)

@@ -7,7 +7,7 @@
 #include <cstdint>
 
 #include "lscan.h"
-#include "lscan_scan_ws2.cuh"
+#include "lscan_scan_ws2.cuh"  // -I paper_1604_04815_b200/csrc
 
 using namespace lscan;
 

@@ -20,7 +20,7 @@ INCLUDE = os.path.join(REPO_DIR, "include")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
 
-SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_lab.cu", "lscan_inst_i32.cu", "lscan_inst_i64.cu",
+SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_inst_i32.cu", "lscan_inst_i64.cu",
            "lscan_inst_f32.cu", "lscan_inst_f64.cu"]
 HEADERS = ["lscan_common.cuh", "lscan_ptx.cuh", "lscan_generic.cuh", "lscan_scan_ws2.cuh", "lscan_dispatch.h",
            "lscan_inst.cuh"]

@@ -49,8 +49,10 @@ def main():
     ap.add_argument("--wide", action="store_true", help="64-bit elements (ws/ws2 configs)")
     args = ap.parse_args()
     L = N.lib()
-    L.ls_lab_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+    LAB = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", "liblscanlab.so"))
+    LAB.ls_lab_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                              ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
+    LAB.ls_lab_run.restype = ctypes.c_int
     n = args.n
     dt = torch.int64 if args.wide else torch.int32
     es = 8 if args.wide else 4
@@ -63,7 +65,7 @@ def main():
     ref = torch.cumsum(x, 0, dtype=dt)
     if args.ncu:
         for _ in range(4):
-            assert L.ls_lab_run(0, 0, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s, ctypes.byref(g)) == 0
+            assert LAB.ls_lab_run(0, 0, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s, ctypes.byref(g)) == 0
         torch.cuda.synchronize()
         return
     res = {"n": n}
@@ -73,7 +75,7 @@ def main():
     for cfg in [int(c) for c in args.cfgs.split(",")]:
         for fl in [int(f) for f in args.flags.split(",")]:
             def step():
-                rc = L.ls_lab_run(cfg, fl | (256 if args.wide else 0), x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s, ctypes.byref(g))
+                rc = LAB.ls_lab_run(cfg, fl | (256 if args.wide else 0), x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s, ctypes.byref(g))
                 assert rc == 0, rc
             ms = timeit(step, args.reps)
             ok = None
