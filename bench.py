@@ -64,6 +64,11 @@ def synthetic(n: int, tok: str, seed) -> np.ndarray:
     return rng.uniform(-1.0, 1.0, size=n).astype(dt)
 
 
+def workload_name(tok: str, n: int) -> str:
+    return (f"{tok} inclusive sum-scan, N=2^{n.bit_length() - 1} per GPU"
+            + (" (BASELINE configs[1])" if n == N_DEFAULT and tok == "i32" else ""))
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -198,17 +203,19 @@ def cub_gelems(tok: str, xd, steps: int, warmup: int):
     return n / (ms * 1e-3) * 1e-9
 
 
-def cpu_reference(tok: str, n: int, samples: int = 3):
+def cpu_reference(tok: str, n: int, budget_s: float = 10.0):
     """The reference algorithm on the host cores: oracle/lscan_oracle.c's
     threaded restatement of chained_scan (B = all hardware threads,
-    L = 65536 as in test_acceptance.py:281-282), on a bounded sample."""
+    L = 65536 as in test_acceptance.py:281-282), repeated on the bench
+    workload for about ``budget_s`` seconds of CPU work (median reported)."""
     import oracle  # bench's cpu_baseline leg only
     cores = os.cpu_count() or 1
     x = synthetic(n, tok, [0, n])
     y = np.empty_like(x)
     oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)  # warm
     ts = []
-    for _ in range(samples):
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(ts) < 3:
         t0 = time.perf_counter()
         oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)
         ts.append(time.perf_counter() - t0)
@@ -218,10 +225,11 @@ def cpu_reference(tok: str, n: int, samples: int = 3):
         t0 = time.perf_counter()
         oracle.sequential_scan(xs)
         seq_t.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
     return {
-        "value": n / min(ts) * 1e-9, "unit": "Gelem/s", "cores": cores, "kind": "port",
+        "value": n / med * 1e-9, "unit": "Gelem/s", "cores": cores, "kind": "port",
         "sample": f"{tok} N={n} (the bench workload), C restatement of chained_scan, B={cores} threads, "
-                  f"L=65536, best of {samples} ({min(ts):.3f} s)",
+                  f"L=65536, median of {len(ts)} runs over {sum(ts):.1f} s",
         "numpy_sequential_gelems": xs.size / min(seq_t) * 1e-9,
         "cpu_model": _cpu_model(),
     }
@@ -350,8 +358,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": tok,
         "data": "synthetic (reference generate_input recipe: full-range ints / U[-1,1] floats, seed [rank, n])",
-        "config": {"workload": f"{tok} inclusive sum-scan, N=2^{n.bit_length() - 1} per GPU"
-                               + (" (BASELINE configs[1])" if n == N_DEFAULT and tok == "i32" else ""),
+        "config": {"workload": workload_name(tok, n),
                    "n_per_gpu": n, "n_total": total_elems, "op": "add",
                    "l2": "inputs (>=1 GiB) larger than L2 (126 MB); no flush",
                    "parallelism": (f"cyclic{world}" if multi_path and multi_path.startswith("fused")
@@ -483,9 +490,10 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     x = synthetic(n, tok, [0, n])
     y = np.empty_like(x)
-    # bounded: at most ~3 timed samples + 1 warm-up of the full workload
-    k = min(steps, 3)
-    for _ in range(min(warm, 1)):
+    # each step: one run of the reference algorithm over the whole workload
+    # (~0.03-0.5 s on a many-core host), W untimed warm-ups first
+    k = steps
+    for _ in range(warm):
         oracle.c_chained_scan(x, out=y, block_len=65536, workers=cores)
     ts = []
     for _ in range(k):
@@ -496,10 +504,11 @@ def run_reference(args):
     value = n / t * 1e-9
     out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gelem/s",
-        "n_gpus": args.gpus, "steps": k, "warmup": min(warm, 1), "ms_per_step": round(t * 1e3, 3),
+        "n_gpus": args.gpus, "steps": k, "warmup": warm, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": tok,
         "data": "synthetic (reference generate_input recipe)",
-        "config": {"workload": f"{tok} inclusive sum-scan, N=2^{n.bit_length() - 1}", "n_per_gpu": n},
+        "config": {"workload": workload_name(tok, n), "n_per_gpu": n, "n_total": n, "op": "add",
+                   "l2": "inputs (>=1 GiB) larger than L2 (126 MB); no flush", "parallelism": "host threads"},
         "cpu_baseline": {"value": round(value, 4), "unit": "Gelem/s", "cores": cores, "kind": "port",
                          "sample": f"{tok} N={n}, C restatement of chained_scan (oracle/lscan_oracle.c), "
                                    f"B={cores} threads, L=65536, median of {k}",
