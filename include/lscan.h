@@ -162,6 +162,13 @@ ls_status ls_debug_config(int64_t spin_budget, int64_t corrupt_block, int protoc
  * Process-wide; (0, 0, -1) disarms. */
 ls_status ls_debug_perturb(int64_t reducer_delay_ns, int64_t scanner_delay_ns, int64_t stall_tile);
 
+/* Slot handshake stress (the reference's acceptance criterion 4,
+ * test_acceptance.py:146-196, on the device): one writer publishes `count`
+ * slots of dtype dt while reader_ctas x 128 threads re-read them; out[0] =
+ * reads, out[1] = torn pairs seen (must be 0), out[2] = published slots seen
+ * unpublished again by the same reader (must be 0).  Synchronous. */
+ls_status ls_debug_slot_stress(ls_dtype dt, int64_t count, int reader_ctas, int64_t stats_out[3]);
+
 /* Reads and clears the device error word of a workspace (synchronises). */
 ls_status ls_workspace_error(void *ws, size_t ws_bytes, void *stream);
 

@@ -48,7 +48,7 @@ EXPORTED = [
     "ls_inclusive_sum_host", "ls_debug_config", "ls_debug_perturb",
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
     "ls_query_config", "ls_launch_count", "ls_xchg_bytes", "ls_inclusive_scan_multi", "ls_exclusive_scan_multi",
-    "ls_device_alloc", "ls_device_free", "ls_ipc_get_handle", "ls_ipc_open", "ls_ipc_close",
+    "ls_device_alloc", "ls_device_free", "ls_ipc_get_handle", "ls_ipc_open", "ls_ipc_close", "ls_debug_slot_stress",
 ]
 
 
@@ -139,6 +139,7 @@ def lib():
             "ls_ipc_get_handle": (ci, [vp, vp]),
             "ls_ipc_open": (ci, [vp, ctypes.POINTER(ctypes.c_void_p)]),
             "ls_ipc_close": (ci, [vp]),
+            "ls_debug_slot_stress": (ci, [ci, i64, ci, ctypes.POINTER(ctypes.c_int64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -522,6 +522,34 @@ ls_status ls_debug_perturb(int64_t reducer_delay_ns, int64_t scanner_delay_ns, i
     return LS_OK;
 }
 
+ls_status ls_debug_slot_stress(ls_dtype dt, int64_t count, int reader_ctas, int64_t stats_out[3]) {
+    if (!valid_dtype(dt) || count < 128 || reader_ctas < 1 || reader_ctas > 1024 || !stats_out)
+        return fail(LS_ERR_INVALID_ARG, "bad stress arguments");
+    const size_t sw = elem_size(dt) == 4 ? 8 : 16;
+    void *buf = nullptr;
+    const size_t bytes = 64 + (size_t)count * sw;
+    LS_CUDA(cudaMalloc(&buf, bytes), "cudaMalloc");
+    ls_status st = LS_OK;
+    do {
+        cudaError_t e = cudaMemset(buf, 0, bytes);
+        if (e != cudaSuccess) { st = cuda_fail(e, "memset"); break; }
+        unsigned long long *stats = static_cast<unsigned long long *>(buf);
+        int *done = reinterpret_cast<int *>(static_cast<uint8_t *>(buf) + 32);
+        uint64_t *slots = reinterpret_cast<uint64_t *>(static_cast<uint8_t *>(buf) + 64);
+        // the stress needs the writer and the readers co-resident: a few CTAs only
+        K(dt).launch_stress(slots, count, 0x5eedu, done, stats, reader_ctas, 0);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { st = cuda_fail(e, "slot stress kernel"); break; }
+        unsigned long long h[3];
+        e = cudaMemcpy(h, stats, sizeof h, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { st = cuda_fail(e, "read stress stats"); break; }
+        for (int i = 0; i < 3; ++i) stats_out[i] = (int64_t)h[i];
+    } while (0);
+    cudaFree(buf);
+    return st;
+}
+
 ls_status ls_workspace_error(void *ws, size_t ws_bytes, void *stream) {
     ls_status st = check_ws_header(ws, ws_bytes, kSlotBase);
     if (st != LS_OK) return st;

@@ -42,6 +42,8 @@ struct DtypeKernels {
     const void *reduce_fn[kNumOps];
     void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s);
     void (*launch_carry)(int op, const void *totals, int64_t rank, void *carry_out, cudaStream_t s);
+    void (*launch_stress)(uint64_t *slots, int64_t count, uint32_t tag, int *writer_done, unsigned long long *stats,
+                          int readers, cudaStream_t s);
 };
 
 const DtypeKernels &kernels_i32();

@@ -286,3 +286,62 @@ __global__ void carry_kernel(const T *totals, int64_t rank, T *carry_out) {
 }
 
 }  // namespace lscan
+
+namespace lscan {
+
+// ------------------------------------------------------------------------------
+// Slot handshake stress (the device analogue of the reference's C4,
+// test_acceptance.py:146-196 / test_chained.py:287-323): one writer thread
+// publishes `count` fresh slots in order with known values while reader warps
+// chase it, each re-reading its own window of 64 slots until the writer is done
+// (plus one final pass).  A reader that sees a slot's tag must see exactly the
+// written value (no torn pair: for 64-bit T the two tagged halves), and a slot
+// once seen published must stay published for that reader (flags monotone).
+// stats[0] = reads, stats[1] = torn, stats[2] = regressions.
+__device__ __forceinline__ uint64_t stress_value(int64_t i) {
+    return ((uint64_t)i * 2654435761ull) & ((1ull << 62) - 1);
+}
+
+template <typename T>
+__global__ void slot_stress_kernel(uint64_t *slots, int64_t count, uint32_t tag, volatile int *writer_done,
+                                   unsigned long long *stats) {
+    using S = Slot<T>;
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            for (int64_t i = 0; i < count; ++i) {
+                S::publish(slots, i, tag, (T)stress_value(i));
+                if ((i & 255) == 255) __nanosleep(200);
+            }
+            __threadfence();
+            *writer_done = 1;
+        }
+        return;
+    }
+    const int64_t reader = (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
+    const int64_t base = (reader * 64) % (count > 64 ? count - 64 : 1);
+    uint64_t seen = 0;
+    unsigned long long reads = 0, torn = 0, regress = 0;
+    bool finishing = false;
+    while (true) {
+        if (*writer_done) finishing = true;
+        for (int b = 0; b < 64; ++b) {
+            uint64_t w[S::W];
+            T v;
+            S::load(slots, base + b, w);
+            const bool valid = S::decode(w, tag, v);
+            ++reads;
+            if (valid) {
+                if (v != (T)stress_value(base + b)) ++torn;
+                seen |= 1ull << b;
+            } else if (seen & (1ull << b)) {
+                ++regress;
+            }
+        }
+        if (finishing) break;
+    }
+    atomicAdd(&stats[0], reads);
+    atomicAdd(&stats[1], torn);
+    atomicAdd(&stats[2], regress);
+}
+
+}  // namespace lscan

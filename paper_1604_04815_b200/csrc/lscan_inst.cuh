@@ -59,6 +59,12 @@ void launch_carry_t(int op, const void *totals, int64_t rank, void *carry_out, c
 }
 
 template <typename T>
+void launch_stress_t(uint64_t *slots, int64_t count, uint32_t tag, int *writer_done, unsigned long long *stats,
+                     int readers, cudaStream_t s) {
+    slot_stress_kernel<T><<<1 + readers, 128, 0, s>>>(slots, count, tag, writer_done, stats);
+}
+
+template <typename T>
 DtypeKernels make_kernels() {
     DtypeKernels k{};
     fill_op<T, OpAdd>(k);
@@ -66,6 +72,7 @@ DtypeKernels make_kernels() {
     fill_op<T, OpMin>(k);
     k.launch_reduce = &launch_reduce_t<T>;
     k.launch_carry = &launch_carry_t<T>;
+    k.launch_stress = &launch_stress_t<T>;
     return k;
 }
 

@@ -47,9 +47,10 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--ncu", action="store_true", help="few launches of cfg 0 only (for profiling)")
     ap.add_argument("--wide", action="store_true", help="64-bit elements (ws/ws2 configs)")
+    ap.add_argument("--labso", default="liblscanlab.so", help="lab library in bench_support/_build")
     args = ap.parse_args()
     L = N.lib()
-    LAB = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", "liblscanlab.so"))
+    LAB = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", args.labso))
     LAB.ls_lab_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                              ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
     LAB.ls_lab_run.restype = ctypes.c_int

@@ -113,3 +113,17 @@ def test_streams_are_independent(S, oracle_lib):
     torch.cuda.synchronize()
     assert np.array_equal(y1.cpu().numpy(), oracle_lib.c_sequential_scan(x1)[0])
     assert np.array_equal(y2.cpu().numpy(), oracle_lib.c_sequential_scan(x2)[0])
+
+
+@pytest.mark.parametrize("tok,code", [("i32", 0), ("i64", 1), ("f32", 2), ("f64", 3)])
+def test_slot_handshake_stress(S, tok, code):
+    # the reference's C4 (test_acceptance.py:146-196) on the device: >= 1e6
+    # reads of slots being published, zero torn pairs, flags monotone
+    import ctypes
+
+    from paper_1604_04815_b200 import _native as N
+    out = (ctypes.c_int64 * 3)()
+    assert N.lib().ls_debug_slot_stress(code, 150_000, 32, out) == 0, N.last_detail()
+    reads, torn, regress = out
+    assert reads >= 1_000_000
+    assert torn == 0 and regress == 0
