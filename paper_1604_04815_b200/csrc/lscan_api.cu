@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -70,6 +71,16 @@ ls_status cuda_fail(cudaError_t e, const char *what) {
 
 // below this size a misaligned input stays on the generic kernel (one launch)
 constexpr int64_t kSplitMinElems = 1 << 20;
+
+// LSCAN_NO_COOP=1: plain launches (lab measurement of the cooperative-launch
+// cost).  The grid never exceeds the co-resident capacity either way.
+bool cooperative_launch() {
+    static const bool coop = [] {
+        const char *e = getenv("LSCAN_NO_COOP");
+        return !(e && e[0] == '1');
+    }();
+    return coop;
+}
 
 bool valid_dtype(ls_dtype dt) { return dt >= LS_I32 && dt <= LS_F64; }
 bool valid_op(ls_op op) { return op >= LS_OP_ADD && op <= LS_OP_MIN; }
@@ -240,6 +251,7 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    cfg.numAttrs = cooperative_launch() ? 1 : 0;
     LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "scan kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return LS_OK;

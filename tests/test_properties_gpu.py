@@ -1,0 +1,72 @@
+"""Size-independent properties at the BASELINE sizes (2^28 and the top of
+the sweep, 2^30), checked on the device without a CPU oracle: linearity of
+the wrapping sum, the difference identity, inclusive - exclusive = x,
+carry splitting, max idempotence/monotonicity, and the float envelope
+against a float64 device cumsum (bench.py:49, :90-114)."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    from paper_1604_04815_b200 import scan
+    return scan
+
+
+def rand_int(n, dtype, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    info = torch.iinfo(dtype)
+    return torch.randint(info.min, info.max, (n,), dtype=dtype, device="cuda", generator=g)
+
+
+@pytest.mark.parametrize("dtype,n", [(torch.int32, 1 << 28), (torch.int64, 1 << 28), (torch.int32, 1 << 30)])
+def test_integer_properties_full_size(S, dtype, n):
+    a = rand_int(n, dtype, 1)
+    ya = S.inclusive_scan(a)
+    # difference identity (wrapping): y[0] = x[0], y[j] - y[j-1] = x[j]
+    assert torch.equal(ya[1:] - ya[:-1], a[1:]) and ya[0] == a[0]
+    # inclusive - exclusive = x
+    ea = S.exclusive_scan(a)
+    assert ea[0] == 0 and torch.equal(ya - ea, a)
+    # linearity of the wrapping sum
+    b = rand_int(n, dtype, 2)
+    yb = S.inclusive_scan(b)
+    del ea
+    assert torch.equal(ya + yb, S.inclusive_scan(a + b))
+    del b, yb
+    # carry splitting at an arbitrary point
+    k = n // 3 + 12345
+    tot = torch.empty(1, dtype=dtype, device="cuda")
+    head = S.inclusive_scan(a[:k].clone(), total_out=tot)
+    tail = S.inclusive_scan(a[k:].clone(), carry_in=tot)
+    assert torch.equal(torch.cat([head, tail]), ya)
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64, torch.float32, torch.float64])
+def test_max_min_properties_full_size(S, dtype):
+    n = 1 << 28
+    x = rand_int(n, dtype, 3) if not dtype.is_floating_point else torch.rand(n, dtype=dtype, device="cuda") * 2 - 1
+    m = S.inclusive_scan(x, op="max")
+    assert torch.equal(S.inclusive_scan(m, op="max"), m)      # idempotent
+    assert bool((m[1:] >= m[:-1]).all())                        # monotone
+    assert torch.equal(m, torch.cummax(x, 0).values)
+    mn = S.inclusive_scan(x, op="min")
+    assert torch.equal(mn, torch.cummin(x, 0).values)
+
+
+@pytest.mark.parametrize("dtype,eps", [(torch.float32, 1e-5), (torch.float64, 1e-12)])
+def test_float_envelope_full_size(S, dtype, eps):
+    n = 1 << 28
+    x = torch.rand(n, dtype=dtype, device="cuda") * 2 - 1
+    y = S.inclusive_scan(x).double()
+    ref = torch.cumsum(x.double(), 0)
+    tol = eps * torch.cumsum(x.double().abs(), 0)
+    assert bool(((y - ref).abs() <= tol).all())
+    # deterministic association: bit-identical on a second run
+    assert torch.equal(S.inclusive_scan(x).double(), y)
