@@ -70,3 +70,26 @@ def test_float_envelope_full_size(S, dtype, eps):
     assert bool(((y - ref).abs() <= tol).all())
     # deterministic association: bit-identical on a second run
     assert torch.equal(S.inclusive_scan(x).double(), y)
+
+
+@pytest.mark.slow
+def test_two_pow_33_single_gpu(S):
+    # BASELINE configs[4] is 2^33 i32 sharded over GPUs; one B200 holds it
+    # whole (32 GiB in + 32 GiB out): the kernel's 64-bit indexing at 2^33
+    # elements / 2^20 tiles, checked chunk by chunk with the exact
+    # difference identity and the chunk-boundary carries
+    n = 1 << 33
+    free, _ = torch.cuda.mem_get_info()
+    if free < 72 * (1 << 30):
+        pytest.skip("needs ~72 GiB of free device memory")
+    x = torch.empty(n, dtype=torch.int32, device="cuda")
+    step = 1 << 28
+    for i in range(0, n, step):
+        x[i:i + step] = rand_int(step, torch.int32, i // step)
+    y = S.inclusive_scan(x)
+    prev = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for i in range(0, n, step):
+        xs, ys = x[i:i + step], y[i:i + step]
+        assert torch.equal(ys[1:] - ys[:-1], xs[1:])
+        assert torch.equal(ys[:1], prev + xs[:1])
+        prev = ys[-1:].clone()
