@@ -169,3 +169,39 @@ def test_repeated_calls_alternate_parity(env, oracle_lib):
                                   oracle_lib.sequential_scan(glob, op=op)), (i, op)
     finally:
         v.close()
+
+
+@pytest.mark.slow
+def test_two_pow_33_over_eight_virtual_gpus(env):
+    # BASELINE configs[4]: 2^33 i32 over 8 GPUs, here 8 virtual GPUs of one
+    # B200 (2^30 elements each, 64 GiB in + out), checked on the device with
+    # the exact difference identity inside stripes and the stripe heads
+    # against the block-cyclic prefix of the stripe sums
+    N, S, _ = env
+    W, n = 8, 1 << 30
+    free, _ = torch.cuda.mem_get_info()
+    if free < 72 * (1 << 30):
+        pytest.skip("needs ~72 GiB of free device memory")
+    g = torch.Generator(device="cuda").manual_seed(7)
+    xs = [torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g) for _ in range(W)]
+    v = VirtualGPUs(env, W, torch.int32, n)
+    try:
+        ys, tots = v(xs)
+    finally:
+        v.close()
+    stripe = v.grid * S.query_config(torch.int32, n)["tile_elems"]
+    rounds = (n + stripe - 1) // stripe
+    sums = torch.empty(rounds, W, dtype=torch.int64, device="cuda")
+    for r in range(W):
+        for k in range(rounds):
+            sums[k, r] = xs[r][k * stripe:(k + 1) * stripe].sum(dtype=torch.int64)
+    order = sums.reshape(-1).to(torch.int32).to(torch.int64)
+    excl = (torch.cumsum(order, 0) - order).reshape(rounds, W).to(torch.int32)
+    for r in range(W):
+        x, y = xs[r], ys[r]
+        for k in range(rounds):
+            lo, hi = k * stripe, min(n, (k + 1) * stripe)
+            assert torch.equal(y[lo + 1:hi] - y[lo:hi - 1], x[lo + 1:hi])
+            assert y[lo] == (excl[k, r] + x[lo]).to(torch.int32)
+    total = order.sum().to(torch.int32)
+    assert all(t.item() == total.item() for t in tots)
