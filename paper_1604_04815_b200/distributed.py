@@ -149,14 +149,26 @@ class CyclicScan:
         dist.all_gather_object(handles, handle.raw, group=group)
         self._opened = []
         peers = []
-        for g, h in enumerate(handles):
-            if g == self.rank:
-                peers.append(self.xchg)
-                continue
-            p = ctypes.c_void_p()
-            raise_for_status(L.ls_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
-            self._opened.append(p.value)
-            peers.append(p.value)
+        err = None
+        try:
+            for g, h in enumerate(handles):
+                if g == self.rank:
+                    peers.append(self.xchg)
+                    continue
+                p = ctypes.c_void_p()
+                raise_for_status(L.ls_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
+                self._opened.append(p.value)
+                peers.append(p.value)
+        except Exception as e:  # noqa: BLE001 - every rank must learn about it
+            err = e
+        # all ranks agree before anyone can block on a peer (a rank that could
+        # not map its peers must not leave the others waiting in a barrier)
+        ok = torch.tensor([0 if err else 1], device=self.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if not ok.item():
+            self.close()
+            raise RuntimeError(f"peer mapping failed on some rank: {err!r}" if err else
+                               "peer mapping failed on another rank")
         self.peers = torch.tensor(peers, dtype=torch.int64, device=self.device)
         # nobody may push into a peer's region before that peer zeroed it
         dist.barrier(group=group)
@@ -184,10 +196,10 @@ class CyclicScan:
     def close(self):
         L = self._N.lib()
         torch.cuda.synchronize()
-        for p in self._opened:
+        for p in getattr(self, "_opened", []):
             L.ls_ipc_close(p)
         self._opened = []
-        if self.xchg:
+        if getattr(self, "xchg", None):
             L.ls_device_free(self.xchg)
             self.xchg = None
 
