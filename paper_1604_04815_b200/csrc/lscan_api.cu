@@ -232,7 +232,6 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     p.spin_budget = dbg.spin_budget;
     p.corrupt_tile = dbg.corrupt;
     p.protocol_checks = dbg.protocol;
-    p.experiment = 0;
     p.delay_red_ns = dbg.delay_red_ns;
     p.delay_scan_ns = dbg.delay_scan_ns;
     // a stalled tile without a watchdog would hang the chain forever

@@ -129,7 +129,6 @@ struct ScanParams {
     int64_t spin_budget;    // 0 = unlimited
     int64_t corrupt_tile;   // -1 = off
     int protocol_checks;
-    int experiment;         // lab-only bits: 1 = skip the look-back (timing upper bound, wrong sums)
     int64_t delay_red_ns;   // debug: reducer sleeps this long on tiles t % 3 == 1 (timing perturbation)
     int64_t delay_scan_ns;  // debug: scanners sleep this long on tiles t % 3 == 2
     int64_t stall_tile;     // debug: this tile never publishes its aggregate (needs a spin budget)

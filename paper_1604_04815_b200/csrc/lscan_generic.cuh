@@ -163,9 +163,8 @@ __global__ void __launch_bounds__(THREADS, 1) scan_generic_kernel(const ScanPara
                     S::publish(agg, t, tag, t == p.corrupt_tile ? ident : tile_agg);
             }
             T prefix = ident;
-            const bool has = (p.experiment & 1) ? false
-                                                : round_lookback<T, OP>(agg, rnd, k, c, G, tag, carry_in, lane,
-                                                                        p.spin_budget, hdr, prefix);
+            const bool has = round_lookback<T, OP>(agg, rnd, k, c, G, tag, carry_in, lane, p.spin_budget, hdr,
+                                                   prefix);
             const T incl = has ? OP::apply(prefix, tile_agg) : tile_agg;
             if (lane == 0) {
                 if (c == G - 1 && t + 1 < M) S::publish(rnd, k, tag, incl);
