@@ -177,21 +177,65 @@ class CyclicScan:
                  exclusive: bool = False, carry_in: Optional[torch.Tensor] = None,
                  total_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         S, N = self._S, self._N
-        if x.numel() != self.n_local or x.dtype != self.dtype or not x.is_contiguous():
-            raise ValueError("x must be the contiguous local share this scanner was built for")
+        # a call may cover a prefix of the share (the chunks of scan_host): every
+        # GPU passes the same length, a multiple of stripe_elems except at the end
+        if x.numel() > self.n_local or x.dtype != self.dtype or not x.is_contiguous():
+            raise ValueError("x must be a contiguous (part of the) local share this scanner was built for")
         if out is None:
             out = torch.empty_like(x)
         stream = torch.cuda.current_stream(x.device)
         L = N.lib()
         ws = S.workspace(x.device, stream, L.ls_workspace_bytes(self.dt, self.n_local))
         fn = L.ls_exclusive_scan_multi if exclusive else L.ls_inclusive_scan_multi
-        rc = fn(S.op_code(op), self.dt, x.data_ptr(), out.data_ptr(), self.n_local,
+        rc = fn(S.op_code(op), self.dt, x.data_ptr(), out.data_ptr(), x.numel(),
                 None if carry_in is None else carry_in.data_ptr(),
                 None if total_out is None else total_out.data_ptr(), ws.data_ptr(), ws.numel(),
                 self.rank, self.world, self.xchg, self.xbytes, self.peers.data_ptr(), self.grid,
                 stream.cuda_stream)
         self._raise(rc)
         return out
+
+    def scan_host(self, xh: torch.Tensor, yh: torch.Tensor, *, op: str = "add", exclusive: bool = False,
+                  stripes_per_chunk: int = 8) -> torch.Tensor:
+        """End to end from host memory: this GPU's share ``xh`` (pinned CPU
+        tensor) -> ``yh``.  The share is streamed in chunks of whole stripes
+        (chunk c of every GPU is one contiguous segment of the global array),
+        each chunk a collective cyclic scan carrying the previous chunk's
+        global total, with copy-in, scan and copy-out overlapped on three
+        streams.  Collective: every GPU calls it with the same sizes."""
+        n = xh.numel()
+        if n != self.n_local or yh.numel() != n or xh.dtype != self.dtype or yh.dtype != self.dtype:
+            raise ValueError("xh / yh must be this scanner's local share")
+        chunk = max(1, stripes_per_chunk) * self.stripe_elems
+        nch = (n + chunk - 1) // chunk
+        nb = 3
+        bufs = [torch.empty(min(chunk, n), dtype=self.dtype, device=self.device) for _ in range(min(nb, nch))]
+        carry = torch.empty(2, dtype=self.dtype, device=self.device)
+        s_in, s_comp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in bufs]
+        ev_comp = [torch.cuda.Event() for _ in bufs]
+        ev_out = [torch.cuda.Event() for _ in bufs]
+        s_in.wait_stream(torch.cuda.current_stream())
+        for c in range(nch):
+            b = c % len(bufs)
+            lo, hi = c * chunk, min(n, (c + 1) * chunk)
+            d = bufs[b][:hi - lo]
+            if c >= len(bufs):
+                s_in.wait_event(ev_out[b])
+            with torch.cuda.stream(s_in):
+                d.copy_(xh[lo:hi], non_blocking=True)
+                ev_in[b].record(s_in)
+            s_comp.wait_event(ev_in[b])
+            with torch.cuda.stream(s_comp):
+                self(d, d, op=op, exclusive=exclusive, carry_in=carry[(c - 1) % 2:(c - 1) % 2 + 1] if c else None,
+                     total_out=carry[c % 2:c % 2 + 1])
+                ev_comp[b].record(s_comp)
+            s_out.wait_event(ev_comp[b])
+            with torch.cuda.stream(s_out):
+                yh[lo:hi].copy_(d, non_blocking=True)
+                ev_out[b].record(s_out)
+        s_out.synchronize()
+        return yh
 
     def close(self):
         L = self._N.lib()

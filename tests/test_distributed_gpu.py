@@ -98,3 +98,40 @@ def test_cyclic_scan_world_one(S, oracle_lib):
                 sc.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_cyclic_scan_host_pipeline_world_one(S, oracle_lib):
+    # CyclicScan.scan_host: chunks of whole stripes, carry chained through the
+    # global totals, copies overlapped — equals the one-shot scan
+    import torch.distributed as dist
+
+    from paper_1604_04815_b200.distributed import CyclicScan
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        for tok, tdt in (("i32", torch.int32), ("f64", torch.float64)):
+            sc = CyclicScan(tdt, 1)  # probe the stripe size
+            stripe = sc.stripe_elems
+            sc.close()
+            n = 7 * stripe + 12345
+            x = oracle_lib.generate_input(n, tok, [4, 4])
+            sc = CyclicScan(tdt, n)
+            try:
+                xp = torch.from_numpy(x).pin_memory()
+                yp = torch.empty_like(xp).pin_memory()
+                sc.scan_host(xp, yp, stripes_per_chunk=2)
+                ref = oracle_lib.c_sequential_scan(x)[0]
+                if tok[0] == "i":
+                    assert np.array_equal(yp.numpy(), ref)
+                else:
+                    assert oracle_lib.validate_output(x, yp.numpy(), ref=ref) is None
+                sc.scan_host(xp, yp, exclusive=True, op="max", stripes_per_chunk=3)
+                assert np.array_equal(yp.numpy(), oracle_lib.exclusive_scan(x, "max"))
+            finally:
+                sc.close()
+    finally:
+        dist.destroy_process_group()
