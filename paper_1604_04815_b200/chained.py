@@ -20,11 +20,15 @@ copy-out overlapped.  There is no CPU path.
 ``ChainConfig`` keeps the reference's fields (chained.py:205-234).  On the
 GPU, ``b`` (workers) and ``geometry`` (block shape) are decided by the
 device (persistent CTAs = co-resident capacity, compile-time tiles) and are
-accepted for compatibility; ``spin_budget``, ``corrupt_slot`` and
-``protocol_checks`` map onto the device watchdog / fault injection /
-publish-once check and raise the reference's ``LivenessError`` /
-``ProtocolViolation``; ``on_block`` (a per-block host callback) has no
-device equivalent and is rejected.
+accepted for compatibility — so float add always follows the reference's
+B > 1 contract (the envelope), never the B == 1 bit-exact fold.
+``spin_budget`` and ``corrupt_slot`` map onto the device watchdog and fault
+injection and raise the reference's ``LivenessError``.  ``protocol_checks``
+needs no per-call check: every device slot is written once per call by
+construction (epoch-tagged words); the explicit device check is
+``scan.debug(protocol_checks=True)`` (raises ``ProtocolViolation``).
+``on_block`` (a per-block host callback) has no device equivalent and is
+rejected.
 """
 
 from __future__ import annotations

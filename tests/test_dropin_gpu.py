@@ -68,6 +68,10 @@ def test_multi_chunk_host_pipeline(oracle_lib):
         ye = P.chained_exclusive_scan(P.ScanProblem(x, op))
         if tok == "i32":
             assert np.array_equal(ye, oracle_lib.c_sequential_scan(x, exclusive=True)[0])
+            # in place through the pageable staging path, several chunks
+            buf = x.copy()
+            assert P.chained_scan(P.ScanProblem(buf, op, out=buf)) is buf
+            assert np.array_equal(buf, y)
 
 
 def test_pinned_host_buffers(oracle_lib):
