@@ -12,13 +12,18 @@
 using namespace lscan;
 
 namespace {
-int g_lab_wide = 0;  // 0 = 32-bit elements, 1 = 64-bit
+int g_lab_dtype = 0;  // ls_dtype: 0 i32, 1 i64, 2 f32, 3 f64
 
 template <int SW, int TILE, int STAGES>
 int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t *grid_out) {
-    const bool wide = g_lab_wide == 1;
-    void (*f)(const ScanParams) = wide ? &scan_ws2_kernel<int64_t, OpAdd, SW, TILE, STAGES, false>
-                                       : &scan_ws2_kernel<int32_t, OpAdd, SW, TILE, STAGES, false>;
+    const bool wide = g_lab_dtype == 1 || g_lab_dtype == 3;
+    void (*f)(const ScanParams) = nullptr;
+    switch (g_lab_dtype) {
+    case 1: f = &scan_ws2_kernel<int64_t, OpAdd, SW, TILE, STAGES, false>; break;
+    case 2: f = &scan_ws2_kernel<float, OpAdd, SW, TILE, STAGES, false>; break;
+    case 3: f = &scan_ws2_kernel<double, OpAdd, SW, TILE, STAGES, false>; break;
+    default: f = &scan_ws2_kernel<int32_t, OpAdd, SW, TILE, STAGES, false>; break;
+    }
     const size_t smem = scan_ws2_smem_bytes<int64_t, SW, TILE, STAGES>();
     const int threads = (SW + 3) * 32;
     if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -54,11 +59,11 @@ int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t 
 }
 }  // namespace
 
-// flags bit 8 selects 64-bit elements
+// flags bits 8..9 select the element type (ls_dtype)
 extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n, void *ws, void *stream,
                           int64_t *grid_out) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    g_lab_wide = (flags >> 8) & 1;
+    g_lab_dtype = (flags >> 8) & 3;
     switch (cfg) {
     case 30: return run_ws<16, 32768, 4>(x, y, n, ws, s, grid_out);
     case 31: return run_ws<16, 32768, 5>(x, y, n, ws, s, grid_out);

@@ -43,7 +43,8 @@ def main():
     ap.add_argument("--n", type=int, default=1 << 28)
     ap.add_argument("--cfgs", default="34,40")
     ap.add_argument("--reps", type=int, default=50)
-    ap.add_argument("--wide", action="store_true", help="64-bit elements")
+    ap.add_argument("--wide", action="store_true", help="64-bit elements (same as --dtype i64)")
+    ap.add_argument("--dtype", choices=["i32", "i64", "f32", "f64"], default=None)
     ap.add_argument("--labso", default="liblscanlab.so", help="lab library in bench_support/_build")
     args = ap.parse_args()
     L = N.lib()
@@ -52,27 +53,34 @@ def main():
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
     LAB.ls_lab_run.restype = ctypes.c_int
     n = args.n
-    dt = torch.int64 if args.wide else torch.int32
-    es = 8 if args.wide else 4
-    x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda")
+    tok = args.dtype or ("i64" if args.wide else "i32")
+    code = {"i32": 0, "i64": 1, "f32": 2, "f64": 3}[tok]
+    dt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[tok]
+    es = 4 if tok in ("i32", "f32") else 8
+    if dt.is_floating_point:
+        x = torch.rand(n, dtype=dt, device="cuda") * 2 - 1
+    else:
+        x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda")
     y = torch.empty_like(x)
     ws = torch.zeros(L.ls_workspace_bytes(N.LS_I64, n) * 8, dtype=torch.uint8, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     g = ctypes.c_int64(0)
-    ref = torch.cumsum(x, 0, dtype=dt)
+    ref = torch.cumsum(x, 0, dtype=dt) if not dt.is_floating_point else torch.cumsum(x.double(), 0)
     res = {"n": n, "dtype": str(dt), "lib": args.labso}
     res["torch_copy_gbs"] = round(2 * n * es / (timeit(lambda: y.copy_(x), args.reps) * 1e-3) / 1e9, 1)
     res["torch_cumsum_gelems"] = round(n / (timeit(lambda: torch.cumsum(x, 0, dtype=dt, out=y),
                                                    args.reps) * 1e-3) * 1e-9, 1)
     for cfg in [int(c) for c in args.cfgs.split(",")]:
         def step():
-            rc = LAB.ls_lab_run(cfg, 256 if args.wide else 0, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s,
+            rc = LAB.ls_lab_run(cfg, code << 8, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s,
                                 ctypes.byref(g))
             assert rc == 0, rc
         ms = timeit(step, args.reps)
         res[f"cfg{cfg}_{CFG_NAMES[cfg]}"] = {
             "gelems": round(n / (ms * 1e-3) * 1e-9, 1), "gbs": round(2 * n * es / (ms * 1e-3) / 1e9, 1),
-            "grid": g.value, "ok": bool(torch.equal(y, ref))}
+            "grid": g.value,
+            "ok": bool(torch.equal(y, ref)) if not dt.is_floating_point
+            else bool(((y.double() - ref).abs() <= 1e-4 * torch.cumsum(x.double().abs(), 0)).all())}
     print(json.dumps(res, indent=1))
 
 
