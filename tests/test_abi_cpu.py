@@ -128,3 +128,31 @@ def test_shard_bounds():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         shard_bounds(10, 2, 2)
+
+
+def _build_c_demo(tmp_path):
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc unavailable")
+    exe = tmp_path / "c_abi_demo"
+    cmd = [gcc, "-O2", "-Wall", "-Werror", f"-I{N.INCLUDE}", "-I/usr/local/cuda/include",
+           os.path.join(N.REPO_DIR, "examples", "c_abi_demo.c"), f"-L{N.LIB_DIR}", "-llscan",
+           "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{N.LIB_DIR}", "-o", str(exe)]
+    subprocess.run(cmd, check=True)
+    return exe
+
+
+def test_c_demo_compiles_against_the_header(tmp_path):
+    # the ABI is consumable from plain C with the header alone
+    assert _build_c_demo(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_c_demo_runs(tmp_path):
+    import subprocess
+    exe = _build_c_demo(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "c_abi_demo ok" in r.stdout
