@@ -175,8 +175,10 @@ def time_device(fn, steps, warmup, stream, dist=None):
     return ms
 
 
-def cub_gelems(tok: str, xd, steps: int, warmup: int):
-    """Side reference: cub::DeviceScan::InclusiveSum on the same buffers."""
+def cub_gelems(tok: str, xd, steps: int, warmup: int, graph: bool = False):
+    """Side reference: cub::DeviceScan::InclusiveSum on the same buffers.
+    ``graph``: the K launches replayed from one CUDA graph (device time only,
+    as ``scripts/sweep.py`` also times ours)."""
     import ctypes
 
     import torch
@@ -196,10 +198,24 @@ def cub_gelems(tok: str, xd, steps: int, warmup: int):
 
     def step():
         rc = L.cub_inclusive_sum(code, xd.data_ptr(), yd.data_ptr(), n, temp.data_ptr(), ctypes.byref(tb),
-                                 s.cuda_stream)
+                                 torch.cuda.current_stream().cuda_stream)
         assert rc == 0
 
-    ms = time_device(step, steps, warmup, s)
+    if graph:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(s)
+        with torch.cuda.stream(gs):
+            step()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(steps):
+                    step()
+        torch.cuda.synchronize()
+        g.replay()
+        ms = time_device(g.replay, 1, 0, s) / steps
+    else:
+        ms = time_device(step, steps, warmup, s)
     return n / (ms * 1e-3) * 1e-9
 
 

@@ -1,0 +1,98 @@
+// cluster_lab.cu — laboratory for the small-n latency kernel (NOT the
+// product): geometry variants of lscan::scan_cluster_kernel and a plain
+// load/store kernel of the same shape (the floor for "read 4 vectors per
+// thread, write them back"), launched with one cluster per call.
+//
+//   lab_cluster(variant, x, y, n, ws, coop, stream) -> 0 / CUDA error code
+//     0: 256 threads, 4 rows (product)    1: 512 threads, 4 rows
+//     2: 256 threads, 8 rows              3: 256 threads, 2 rows
+//     4: copy 1024 x 4 rows               5: copy 256 x 4 rows
+//   lab_block_elems(variant) -> elements per block (int32)
+#include <cuda_runtime.h>
+
+#include "lscan_cluster.cuh"
+
+using namespace lscan;
+
+template <int THREADS, int V>
+__global__ void __launch_bounds__(THREADS, 1) copy_kernel(const ScanParams p) {
+    constexpr int WARP_VECS = 32 * V;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t0 = (int64_t)blockIdx.x * (THREADS / 32) * WARP_VECS * 4;
+    const int64_t valid = p.n - t0;
+    const int32_t *x = static_cast<const int32_t *>(p.x) + t0;
+    int32_t *y = static_cast<int32_t *>(p.y) + t0;
+    uint4 d[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * 4;
+        d[j] = e0 + 4 <= valid ? ldg128(x + e0) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * 4;
+        if (e0 + 4 <= valid) stg128_v4(y + e0, d[j]);
+    }
+}
+
+namespace {
+struct Var {
+    void (*fn)(const ScanParams);
+    int threads;
+    int rows;
+};
+Var var(int v) {
+    switch (v) {
+    case 0: return {&scan_cluster_kernel<int32_t, OpAdd, false, 4, 256, 4>, 256, 4};
+    case 1: return {&scan_cluster_kernel<int32_t, OpAdd, false, 4, 512, 2>, 512, 4};
+    case 2: return {&scan_cluster_kernel<int32_t, OpAdd, false, 8, 256, 4>, 256, 8};
+    case 3: return {&scan_cluster_kernel<int32_t, OpAdd, false, 2, 256, 4>, 256, 2};
+    case 4: return {&copy_kernel<1024, 4>, 1024, 4};
+    case 5: return {&copy_kernel<256, 4>, 256, 4};
+    case 6: return {&scan_cluster_kernel<int32_t, OpAdd, false, 16, 256, 2>, 256, 16};
+    default: return {&scan_cluster_kernel<int32_t, OpAdd, false, 8, 256, 2>, 256, 8};
+    }
+}
+}  // namespace
+
+extern "C" {
+long long lab_block_elems(int v) {
+    const Var w = var(v);
+    return (long long)w.threads * w.rows * 4;
+}
+
+// ws: a zeroed workspace (needed when n spans several clusters); coop: 0
+// drops the cooperative attribute (measures its cost; unsafe in general)
+int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, void *stream) {
+    const Var w = var(v);
+    const long long be = lab_block_elems(v);
+    const long long tiles = (n + be - 1) / be;
+    const int C = (int)(tiles < 16 ? tiles : 16);
+    const long long K = (tiles + C - 1) / C;
+    if (C < 1 || (K > 1 && ((v == 4 || v == 5) || !ws))) return -1;
+    static bool init[8] = {};
+    if (!init[v]) {
+        cudaFuncSetAttribute((const void *)w.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        init[v] = true;
+    }
+    ScanParams p{};
+    p.x = x;
+    p.y = y;
+    p.n = n;
+    p.ws = static_cast<uint8_t *>(ws);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(K * C));
+    cfg.blockDim = dim3((unsigned)w.threads);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (K > 1 && coop) ? 2 : 1;
+    return (int)cudaLaunchKernelEx(&cfg, w.fn, p);
+}
+}

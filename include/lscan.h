@@ -162,6 +162,12 @@ ls_status ls_debug_config(int64_t spin_budget, int64_t corrupt_block, int protoc
  * Process-wide; (0, 0, -1) disarms. */
 ls_status ls_debug_perturb(int64_t reducer_delay_ns, int64_t scanner_delay_ns, int64_t stall_tile);
 
+/* Kernel selection for testing: 0 = automatic (small n on the one-cluster
+ * latency kernel, the rest on the persistent chain), 1 = never use the
+ * cluster kernel, 2 = use it whenever n fits one cluster (even while debug
+ * hooks are armed, which it ignores).  Process-wide. */
+ls_status ls_debug_force_path(int path);
+
 /* Slot handshake stress (the reference's acceptance criterion 4,
  * test_acceptance.py:146-196, on the device): one writer publishes `count`
  * slots of dtype dt while reader_ctas x 128 threads re-read them; out[0] =
@@ -181,6 +187,15 @@ int ls_abi_version(void);
  * per tile, out[3] = pipeline stages, out[4] = resident CTAs per SM,
  * out[5] = SM count. */
 ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]);
+/* The latency kernel (small and mid n) on the current device: out[0] =
+ * blocks per cluster (0 = unavailable), out[1] = elements per block (one
+ * tile each) while n fits one cluster, out[2] = co-resident clusters of the
+ * mid geometry, out[3] = largest n the kernel takes, out[4] = elements per
+ * block of the mid geometry.  A scan of n <= out[3] elements (debug hooks
+ * disarmed) is one launch: carries travel through distributed shared memory
+ * inside a cluster and through epoch-tagged workspace slots between
+ * clusters. */
+ls_status ls_query_cluster(ls_dtype dt, int64_t out[5]);
 /* Number of kernel launches this process has issued through the library. */
 int64_t ls_launch_count(void);
 

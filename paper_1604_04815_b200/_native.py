@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
 
 SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_inst_i32.cu", "lscan_inst_i64.cu",
            "lscan_inst_f32.cu", "lscan_inst_f64.cu"]
-HEADERS = ["lscan_common.cuh", "lscan_ptx.cuh", "lscan_generic.cuh", "lscan_scan_ws2.cuh", "lscan_dispatch.h",
+HEADERS = ["lscan_common.cuh", "lscan_ptx.cuh", "lscan_cluster.cuh", "lscan_generic.cuh", "lscan_scan_ws2.cuh", "lscan_dispatch.h",
            "lscan_inst.cuh"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -49,6 +49,7 @@ EXPORTED = [
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
     "ls_query_config", "ls_launch_count", "ls_xchg_bytes", "ls_inclusive_scan_multi", "ls_exclusive_scan_multi",
     "ls_device_alloc", "ls_device_free", "ls_ipc_get_handle", "ls_ipc_open", "ls_ipc_close", "ls_debug_slot_stress",
+    "ls_debug_force_path", "ls_query_cluster",
 ]
 
 
@@ -140,6 +141,8 @@ def lib():
             "ls_ipc_open": (ci, [vp, ctypes.POINTER(ctypes.c_void_p)]),
             "ls_ipc_close": (ci, [vp]),
             "ls_debug_slot_stress": (ci, [ci, i64, ci, ctypes.POINTER(ctypes.c_int64)]),
+            "ls_debug_force_path": (ci, [ci]),
+            "ls_query_cluster": (ci, [ci, ctypes.POINTER(ctypes.c_int64)]),  # out[5]
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -39,6 +39,7 @@ struct DebugCfg {
     int64_t delay_red_ns = 0;
     int64_t delay_scan_ns = 0;
     int64_t stall_tile = -1;
+    int force_path = 0;  // ls_debug_force_path
     bool armed() const { return spin_budget > 0 || corrupt >= 0 || protocol != 0; }
 };
 std::mutex g_dbg_mu;
@@ -82,6 +83,16 @@ bool cooperative_launch() {
     return coop;
 }
 
+// LSCAN_NO_CLUSTER=1: small arrays take the persistent kernel too (lab
+// comparison of the two latency paths)
+bool cluster_path_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LSCAN_NO_CLUSTER");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 bool valid_dtype(ls_dtype dt) { return dt >= LS_I32 && dt <= LS_F64; }
 bool valid_op(ls_op op) { return op >= LS_OP_ADD && op <= LS_OP_MIN; }
 
@@ -118,6 +129,8 @@ struct DevState {
     int occ[4][kNumOps][2][2] = {};  // resident CTAs per SM [dtype][op][excl][fast]
     int occ_multi[4][kNumOps][2] = {};
     int reduce_occ[4][kNumOps] = {};
+    int cluster_max = 0;          // largest schedulable cluster of the latency kernel (0: path off)
+    int cluster_capacity[2] = {};  // co-resident clusters of that size [small, mid] (min over instances)
 };
 std::mutex g_dev_mu;
 std::vector<DevState> g_dev;
@@ -161,6 +174,46 @@ ls_status device_state(DevState **out) {
                 LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.reduce_fn[op], kReduceThreads, 0),
                         "occupancy");
                 d.reduce_occ[dt][op] = std::max(occ, 1);
+                for (int ex = 0; ex < 2; ++ex)
+                    for (int g = 0; g < 2; ++g)
+                        LS_CUDA(cudaFuncSetAttribute((const void *)k.cluster[op][ex][g].fn,
+                                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                                "cudaFuncSetAttribute(non-portable cluster size)");
+            }
+        }
+        // the latency path needs a whole cluster co-resident: 16 blocks where
+        // the GPCs allow it, else the portable 8; and for several clusters,
+        // how many fit at once (the minimum over every instance)
+        d.cluster_max = 0;
+        for (int c : {kClusterMax, 8}) {
+            int cap[2] = {1 << 30, 1 << 30};
+            for (int g = 0; g < 2; ++g)
+                for (int dt = 0; dt < 4; ++dt)
+                    for (int op = 0; op < kNumOps; ++op)
+                        for (int ex = 0; ex < 2; ++ex) {
+                            const Launch &L = K((ls_dtype)dt).cluster[op][ex][g];
+                            cudaLaunchConfig_t cfg = {};
+                            cfg.gridDim = dim3((unsigned)c);
+                            cfg.blockDim = dim3((unsigned)L.threads);
+                            cudaLaunchAttribute attr[1];
+                            attr[0].id = cudaLaunchAttributeClusterDimension;
+                            attr[0].val.clusterDim.x = (unsigned)c;
+                            attr[0].val.clusterDim.y = 1;
+                            attr[0].val.clusterDim.z = 1;
+                            cfg.attrs = attr;
+                            cfg.numAttrs = 1;
+                            int nc = 0;
+                            if (cudaOccupancyMaxActiveClusters(&nc, (const void *)L.fn, &cfg) != cudaSuccess) {
+                                (void)cudaGetLastError();
+                                nc = 0;
+                            }
+                            cap[g] = std::min(cap[g], nc);
+                        }
+            if (cap[0] >= 1 && cap[1] >= 1) {
+                d.cluster_max = c;
+                d.cluster_capacity[0] = cap[0];
+                d.cluster_capacity[1] = cap[1];
+                break;
             }
         }
         d.init = true;
@@ -211,6 +264,74 @@ ls_status identity_fill(ls_op op, ls_dtype dt, void *dst, const void *carry_in, 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LS_CUDA(cudaGetLastError(), "identity fill");
     return LS_OK;
+}
+
+// Small and mid n: one tile per block, clusters of up to d.cluster_max
+// blocks (carries through DSMEM), several clusters co-resident by a
+// cooperative launch (cluster aggregates through epoch-tagged slots).
+// Geometry g: 0 = small tiles (n fits one cluster of them), 1 = mid tiles.
+int cluster_geometry(const DevState &d, ls_dtype dt, int64_t n) {
+    const int64_t te = K(dt).cluster[0][0][0].tile_bytes / elem_size(dt);
+    return n <= te * d.cluster_max ? 0 : 1;
+}
+
+ls_status launch_cluster(const DevState &d, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
+                         const void *carry_in, void *total_out, void *ws, cudaStream_t s, bool excl) {
+    const Launch &L = K(dt).cluster[op][excl][cluster_geometry(d, dt, n)];
+    const int64_t te = L.tile_bytes / elem_size(dt);
+    const int64_t tiles = (n + te - 1) / te;
+    const int C = (int)std::min<int64_t>(tiles, d.cluster_max);
+    const int64_t clusters = (tiles + C - 1) / C;
+    ScanParams p{};
+    p.x = x;
+    p.y = y;
+    p.n = n;
+    p.carry_in = carry_in;
+    p.total_out = total_out;
+    p.ws = static_cast<uint8_t *>(ws);
+    p.num_tiles = tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * C));
+    cfg.blockDim = dim3((unsigned)L.threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    // several clusters wait on each other's aggregates: all must be resident
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = clusters > 1 ? 2 : 1;
+    LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "cluster scan kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return LS_OK;
+}
+
+// largest n the cluster kernel takes: one cluster of small tiles always;
+// mid tiles up to the co-resident capacity and the measured crossover with
+// the persistent kernel (LSCAN_CLUSTER_MAX_BYTES overrides it for labs)
+int64_t cluster_limit(const DevState &d, ls_dtype dt) {
+    static const int64_t max_bytes = [] {
+        const char *e = getenv("LSCAN_CLUSTER_MAX_BYTES");
+        return e ? std::max<int64_t>(0, atoll(e)) : kClusterMaxBytes;
+    }();
+    const int64_t es = elem_size(dt);
+    const int64_t one_small = K(dt).cluster[0][0][0].tile_bytes / es * d.cluster_max;
+    const int64_t coresident = K(dt).cluster[0][0][1].tile_bytes / es * d.cluster_max * d.cluster_capacity[1];
+    return std::max(one_small, std::min(coresident, max_bytes / es));
+}
+
+bool use_cluster(const DevState &d, ls_dtype dt, int64_t n, const DebugCfg &dbg) {
+    // the debug hooks (watchdog, corrupt / stalled tiles, perturbation) live
+    // in the persistent kernel's carry chain: keep those calls on it
+    if (d.cluster_max == 0 || dbg.force_path == 1) return false;
+    if (dbg.force_path != 2 && (!cluster_path_enabled() || dbg.armed() || dbg.delay_red_ns > 0 ||
+                                dbg.delay_scan_ns > 0 || dbg.stall_tile >= 0))
+        return false;
+    return n <= cluster_limit(d, dt);
 }
 
 // One kernel launch of the fast (TMA, 16-byte aligned) or generic path.
@@ -278,7 +399,9 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
     const DebugCfg dbg = debug_snapshot();
 
     const uintptr_t mx = (uintptr_t)x & 15u, my = (uintptr_t)y & 15u;
-    if (mx == 0 && my == 0) {
+    if (use_cluster(*d, dt, n, dbg)) {
+        st = launch_cluster(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl);
+    } else if (mx == 0 && my == 0) {
         st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, true, dbg);
     } else if (mx == my && n >= kSplitMinElems) {
         // x and y share their misalignment (e.g. a slice scanned in place):
@@ -533,6 +656,13 @@ ls_status ls_debug_perturb(int64_t reducer_delay_ns, int64_t scanner_delay_ns, i
     return LS_OK;
 }
 
+ls_status ls_debug_force_path(int path) {
+    if (path < 0 || path > 2) return fail(LS_ERR_INVALID_ARG, "path must be 0, 1 or 2");
+    std::lock_guard<std::mutex> lk(g_dbg_mu);
+    g_dbg.force_path = path;
+    return LS_OK;
+}
+
 ls_status ls_debug_slot_stress(ls_dtype dt, int64_t count, int reader_ctas, int64_t stats_out[3]) {
     if (!valid_dtype(dt) || count < 128 || reader_ctas < 1 || reader_ctas > 1024 || !stats_out)
         return fail(LS_ERR_INVALID_ARG, "bad stress arguments");
@@ -581,6 +711,19 @@ ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]) {
     out[3] = L.stages;
     out[4] = occ;
     out[5] = d->sms;
+    return LS_OK;
+}
+
+ls_status ls_query_cluster(ls_dtype dt, int64_t out[5]) {
+    if (!valid_dtype(dt) || !out) return fail(LS_ERR_INVALID_ARG, "bad arguments");
+    DevState *d = nullptr;
+    ls_status st = device_state(&d);
+    if (st != LS_OK) return st;
+    out[0] = cluster_path_enabled() ? d->cluster_max : 0;
+    out[1] = K(dt).cluster[0][0][0].tile_bytes / elem_size(dt);
+    out[2] = cluster_path_enabled() ? d->cluster_capacity[1] : 0;
+    out[3] = cluster_path_enabled() ? cluster_limit(*d, dt) : 0;
+    out[4] = K(dt).cluster[0][0][1].tile_bytes / elem_size(dt);
     return LS_OK;
 }
 

@@ -1,0 +1,254 @@
+// lscan_cluster.cuh — the latency path (small and mid n): one tile per
+// block, blocks grouped in thread-block clusters, the inter-block carry
+// passed through distributed shared memory inside a cluster and through
+// epoch-tagged global slots between clusters.
+//
+// The reference's chain (chained.py:153-172: block i waits for block i-1's
+// inclusive value) becomes "every block needs the sum of the blocks before
+// it".  Inside a cluster (up to 16 co-scheduled blocks) that exchange is one
+// DSMEM store per (block, later block) pair and one cluster barrier.  Across
+// clusters each cluster publishes its aggregate as soon as its barrier
+// passes — it depends on nothing outside the cluster — and every block folds
+// the aggregates of the clusters before it: one L2 round trip, no serial
+// chain.  All clusters are co-resident (cooperative launch), so the waits
+// cannot deadlock.  With one cluster there are no slots and no epoch at all:
+// launch + one load + the block scan + one cluster barrier + one store.
+//
+// Block b owns tile b (TILE_ELEMS contiguous elements).  Inside
+// the block the layout and the scan are the hot kernel's (Alg. 2/3/5,
+// warp.py:85-169): each warp owns WARP_BYTES contiguous bytes as V rows of
+// 32 lanes x 16-byte vectors; per row a thread-serial fold, a
+// __shfl_up_sync warp scan and a serial row carry; a shared-memory scan of
+// the warp totals; the carry folded in registers and stored with 128-bit
+// stores.  Any element-aligned x / y works: vectors that are misaligned or
+// cross the end of the array fall back to element accesses.
+#pragma once
+#include "lscan_common.cuh"
+
+namespace lscan {
+
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// address of `local` (this CTA's shared memory) in CTA `cta` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t local, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t addr, uint64_t v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+// every thread of every CTA of the cluster; release/acquire orders the DSMEM
+// stores issued before the arrival with the loads after the wait
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void stg128_v4(void *p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ldg128(const void *p) {
+    uint4 v;
+    asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+template <typename T, typename OP, bool EXCL, int V, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanParams p) {
+    constexpr int WARPS = THREADS / 32;
+    constexpr int PER = 16 / (int)sizeof(T);
+    constexpr int WARP_VECS = 32 * V;
+    constexpr int TILE_ELEMS = WARPS * WARP_VECS * PER;
+    using Bits = typename Elem<T>::Bits;
+    using S = Slot<T>;
+
+    __shared__ T warp_tot[WARPS];
+    __shared__ T warp_exc[WARPS];
+    __shared__ Bits cta_agg[kClusterMax];  // aggregates of the lower blocks of this cluster, stored by them
+    __shared__ T block_agg;
+    __shared__ T s_pre;                    // carry (+) clusters before this one (+) blocks before this one
+    __shared__ int s_has;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t r = cluster_ctarank();
+    const uint32_t C = cluster_nctarank();
+    const int64_t b = blockIdx.x;        // tile index
+    const int64_t k = b / C;             // cluster index
+    const int64_t K = gridDim.x / C;     // clusters in the grid
+    const T ident = OP::template identity<T>();
+    const int64_t t0 = b * TILE_ELEMS;
+    int64_t valid = p.n - t0 < TILE_ELEMS ? p.n - t0 : TILE_ELEMS;  // <= 0: a padding block of the last cluster
+    if (valid < 0) valid = 0;
+    const T *x = static_cast<const T *>(p.x) + t0;
+    T *y = static_cast<T *>(p.y) + t0;
+    const bool xv = ((uintptr_t)x & 15u) == 0, yv = ((uintptr_t)y & 15u) == 0;
+    Header *hdr = reinterpret_cast<Header *>(p.ws);
+    const uint32_t tag = K > 1 ? call_tag(hdr) : 0u;
+
+    // ---- load: row j of warp w is vectors w*WARP_VECS + j*32 + lane
+    Regs<T, V> d;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
+        if (xv && e0 + PER <= valid) {
+            d.q[j] = ldg128(x + e0);
+        } else {
+#pragma unroll
+            for (int e = 0; e < PER; ++e) d.e[j * PER + e] = e0 + e < valid ? x[e0 + e] : ident;
+        }
+    }
+
+    // ---- per row: lane-serial fold of the vector, inclusive warp scan
+    T rex[V], rtot[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        T v = d.e[j * PER];
+#pragma unroll
+        for (int e = 1; e < PER; ++e) v = OP::apply(v, d.e[j * PER + e]);
+        const T inc = warp_inclusive_scan<T, OP>(v, lane);
+        rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
+        rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
+    }
+    T rowpre[V];
+    T run = rtot[0];
+    rowpre[0] = ident;
+#pragma unroll
+    for (int j = 1; j < V; ++j) {
+        rowpre[j] = run;
+        run = OP::apply(run, rtot[j]);
+    }
+    if (lane == 0) warp_tot[warp] = run;
+    __syncthreads();
+
+    // ---- warp totals -> exclusive warp prefixes; the block aggregate goes to
+    //      every later block of the cluster (DSMEM), slot r
+    if (warp == 0) {
+        const T wi = warp_inclusive_scan<T, OP>(lane < WARPS ? warp_tot[lane] : ident, lane);
+        const T we = __shfl_up_sync(0xffffffffu, wi, 1);
+        if (lane < WARPS) warp_exc[lane] = we;
+        const T agg = __shfl_sync(0xffffffffu, wi, WARPS - 1);
+        const uint32_t local = smem_u32(&cta_agg[r]);
+        for (uint32_t q = r + 1 + (uint32_t)lane; q < C; q += 32) {
+            const uint32_t a = mapa_shared(local, q);
+            if constexpr (sizeof(T) == 4) st_cluster_u32(a, Elem<T>::bits(agg));
+            else st_cluster_u64(a, Elem<T>::bits(agg));
+        }
+        if (lane == 0) block_agg = agg;
+    }
+    if (C > 1) cluster_sync_all();
+    else __syncthreads();
+
+    // ---- block prefix = carry (+) [clusters 0..k-1] (+) [blocks 0..r-1 of this cluster]
+    if (warp == 0) {
+        // in-cluster part, fixed order
+        bool hc = false;
+        T pc = ident;
+        for (uint32_t q = 0; q < r; ++q) {
+            const T a = Elem<T>::from(cta_agg[q]);
+            pc = hc ? OP::apply(pc, a) : a;
+            hc = true;
+        }
+        bool has = p.carry_in != nullptr;
+        T pre = has ? *static_cast<const T *>(p.carry_in) : ident;
+        if (K > 1) {
+            // the cluster's aggregate depends on nothing outside the cluster:
+            // published at once, so the wait below is one L2 round trip, not
+            // a chain (clusters are co-resident: cooperative launch)
+            uint64_t *slots = reinterpret_cast<uint64_t *>(p.ws + kSlotBase);
+            if (r == C - 1 && lane == 0) S::publish(slots, k, tag, hc ? OP::apply(pc, block_agg) : block_agg);
+            if (k > 0) {
+                T acc = ident;
+                for (int64_t base = 0; base < k; base += 32) {
+                    const int64_t j = base + lane;
+                    T v = ident;
+                    if (j < k) {
+                        uint64_t w[S::W];
+                        S::load(slots, j, w);
+                        while (!S::decode(w, tag, v)) {
+                            __nanosleep(20);
+                            S::load(slots, j, w);
+                        }
+                    }
+                    acc = OP::apply(acc, v);
+                }
+                const T g = warp_reduce_fixed<T, OP>(acc);
+                pre = has ? OP::apply(pre, g) : g;
+                has = true;
+            }
+        }
+        if (r > 0) {
+            pre = has ? OP::apply(pre, pc) : pc;
+            has = true;
+        }
+        if (lane == 0) {
+            s_pre = pre;
+            s_has = has ? 1 : 0;
+            if (p.total_out != nullptr && valid > 0 && t0 + valid == p.n)
+                *static_cast<T *>(p.total_out) = has ? OP::apply(pre, block_agg) : block_agg;
+        }
+    }
+    __syncthreads();
+    bool has0 = s_has != 0;
+    T pre = s_pre;
+    if (warp > 0) {
+        pre = has0 ? OP::apply(pre, warp_exc[warp]) : warp_exc[warp];
+        has0 = true;
+    }
+
+    // ---- fold the carry in registers, store
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        bool has = has0;
+        T acc = pre;
+        if (j > 0) { acc = has ? OP::apply(acc, rowpre[j]) : rowpre[j]; has = true; }
+        if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const T v = d.e[j * PER + e];
+            const bool first = (e == 0 && !has);
+            if (EXCL) {
+                d.e[j * PER + e] = first ? ident : acc;
+                acc = first ? v : OP::apply(acc, v);
+            } else {
+                acc = first ? v : OP::apply(acc, v);
+                d.e[j * PER + e] = acc;
+            }
+        }
+        const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
+        if (yv && e0 + PER <= valid) {
+            stg128_v4(y + e0, d.q[j]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < PER; ++e)
+                if (e0 + e < valid) y[e0 + e] = d.e[j * PER + e];
+        }
+    }
+    // the last block to finish records this call's tag as the workspace epoch
+    // (relaxed: nothing in this grid reads the epoch again, and the next call
+    // starts after this grid has completed)
+    if (K > 1 && tid == 0) {
+        if (atomicAdd(&hdr->done, 1u) == gridDim.x - 1u) {
+            st_relaxed_u32(&hdr->done, 0u);
+            st_relaxed_u32(&hdr->epoch, tag);
+        }
+    }
+}
+
+
+}  // namespace lscan

@@ -2,6 +2,7 @@
 // (included by exactly one lscan_inst_<dtype>.cu each).
 #pragma once
 #include "lscan_dispatch.h"
+#include "lscan_cluster.cuh"
 #include "lscan_generic.cuh"
 #include "lscan_scan_ws2.cuh"
 
@@ -28,8 +29,18 @@ Launch generic_launch() {
             scan_generic_smem_bytes<T, kGenThreads, kGenTileBytes>(), kGenTileBytes, 1};
 }
 
+template <typename T, typename OP, bool EXCL, int V, int MINB>
+Launch cluster_launch() {
+    return {&scan_cluster_kernel<T, OP, EXCL, V, kClusterThreads, MINB>, kClusterThreads, 0,
+            kClusterThreads * V * 16, 1};
+}
+
 template <typename T, typename OP>
 void fill_op(DtypeKernels &k) {
+    k.cluster[OP::code][0][0] = cluster_launch<T, OP, false, kClusterRowsSmall, kClusterMinBlocksSmall>();
+    k.cluster[OP::code][1][0] = cluster_launch<T, OP, true, kClusterRowsSmall, kClusterMinBlocksSmall>();
+    k.cluster[OP::code][0][1] = cluster_launch<T, OP, false, kClusterRowsMid, kClusterMinBlocksMid>();
+    k.cluster[OP::code][1][1] = cluster_launch<T, OP, true, kClusterRowsMid, kClusterMinBlocksMid>();
     k.scan[OP::code][0][1] = fast_launch<T, OP, false>();
     k.scan[OP::code][1][1] = fast_launch<T, OP, true>();
     k.scan[OP::code][0][0] = generic_launch<T, OP, false>();

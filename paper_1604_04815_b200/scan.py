@@ -85,6 +85,28 @@ def op_code(op: str) -> int:
         raise UnsupportedOperatorError(f"unknown operator {op!r}; supported: {', '.join(N.OPS)}") from None
 
 
+# the raw cudaStream_t of a device's current stream, without building a Stream
+# object (torch's own accessor, used by its code generators)
+try:
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover - older torch
+    def _raw_stream(index: int) -> int:
+        return torch.cuda.current_stream(index).cuda_stream
+
+
+_ws_need: Dict[Tuple[int, int], int] = {}
+
+
+def _ws_bytes(dt: int, n: int) -> int:
+    key = (dt, n)
+    b = _ws_need.get(key)
+    if b is None:
+        if len(_ws_need) > 4096:
+            _ws_need.clear()
+        b = _ws_need[key] = N.lib().ls_workspace_bytes(dt, n)
+    return b
+
+
 def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exclusive: bool,
           op: str = "add") -> torch.Tensor:
     _check_1d(x)
@@ -92,7 +114,7 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
     oc = op_code(op)
     if out is None:
         out = torch.empty_like(x, memory_format=torch.contiguous_format)
-    else:
+    elif out is not x:
         _check_1d(out, "out")
         if out.shape != x.shape:
             raise ShapeError("out shape must match input shape")
@@ -101,17 +123,32 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
         if not out.is_contiguous():
             raise ShapeError("out must be contiguous")
     if not x.is_contiguous():
+        if out is x:
+            raise ShapeError("in-place scan needs a contiguous tensor")
         x = x.contiguous()
     n = x.numel()
-    stream = torch.cuda.current_stream(x.device)
-    L = N.lib()
-    ws = workspace(x.device, stream, L.ls_workspace_bytes(dt, n))
-    fn = L.ls_exclusive_scan if exclusive else L.ls_inclusive_scan
-    with torch.cuda.device(x.device):
+    dev = x.device
+    idx = dev.index
+    switch = idx != torch.cuda.current_device()
+    if switch:
+        prev = torch.cuda.current_device()
+        torch.cuda.set_device(idx)
+    try:
+        sp = _raw_stream(idx)
+        ws = _workspaces.get((idx, sp))
+        need = _ws_bytes(dt, n)
+        if ws is None or ws.numel() < need:
+            ws = workspace(dev, torch.cuda.current_stream(dev), need)
+        fn = N.lib().ls_exclusive_scan if exclusive else N.lib().ls_inclusive_scan
         rc = fn(oc, dt, x.data_ptr() if n else None, out.data_ptr() if n else None, n,
-                _scalar_ptr(carry_in, x, "carry_in"), _scalar_ptr(total_out, x, "total_out"),
-                ws.data_ptr(), ws.numel(), stream.cuda_stream)
-    raise_for_status(rc)
+                None if carry_in is None else _scalar_ptr(carry_in, x, "carry_in"),
+                None if total_out is None else _scalar_ptr(total_out, x, "total_out"),
+                ws.data_ptr(), ws.numel(), sp)
+    finally:
+        if switch:
+            torch.cuda.set_device(prev)
+    if rc:
+        raise_for_status(rc)
     return out
 
 
@@ -181,6 +218,37 @@ def query_config(dtype: torch.dtype, n: int) -> dict:
     raise_for_status(N.lib().ls_query_config(dtype_code(dtype), n, out))
     keys = ("grid", "threads", "tile_elems", "stages", "ctas_per_sm", "sms")
     return dict(zip(keys, (int(v) for v in out)))
+
+
+def query_cluster(dtype: torch.dtype) -> dict:
+    """The latency kernel: blocks per cluster (0 = off), elements per block
+    of the small and mid geometries, co-resident mid clusters, the largest n
+    it takes (``max_elems``) and the largest single-cluster n
+    (``one_cluster_elems``)."""
+    import ctypes
+    out = (ctypes.c_int64 * 5)()
+    raise_for_status(N.lib().ls_query_cluster(dtype_code(dtype), out))
+    return {"max_blocks": int(out[0]), "block_elems": int(out[1]), "capacity": int(out[2]),
+            "max_elems": int(out[3]), "one_cluster_elems": int(out[0]) * int(out[1]),
+            "mid_block_elems": int(out[4])}
+
+
+class force_path:
+    """Context manager pinning the kernel choice (tests / labs):
+    ``"auto"``, ``"persistent"`` (never the cluster kernel) or ``"cluster"``
+    (whenever n fits one cluster).  Process-wide."""
+
+    _codes = {"auto": 0, "persistent": 1, "cluster": 2}
+
+    def __init__(self, path: str):
+        self.code = self._codes[path]
+
+    def __enter__(self):
+        raise_for_status(N.lib().ls_debug_force_path(self.code))
+        return self
+
+    def __exit__(self, *exc):
+        N.lib().ls_debug_force_path(0)
 
 
 def check_workspace_error(device: Optional[torch.device] = None) -> None:

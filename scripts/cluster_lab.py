@@ -1,0 +1,56 @@
+"""Graph-timed latency of the small-n kernel variants in
+bench_support/cluster_lab.cu (i32, one cluster per call) next to the
+product path and CUB, to choose the latency kernel's geometry."""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "scripts"))
+from overhead_lab import graph_per_call  # noqa: E402
+
+from paper_1604_04815_b200 import scan as S  # noqa: E402
+
+NAMES = {0: "scan_256x4", 1: "scan_512x4", 2: "scan_256x8", 3: "scan_256x2", 4: "copy_1024x4", 5: "copy_256x4",
+         6: "scan_256x16_minb2", 7: "scan_256x8_minb2"}
+
+
+def main():
+    L = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", "libclusterlab.so"))
+    L.lab_cluster.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                              ctypes.c_int, ctypes.c_void_p]
+    L.lab_block_elems.restype = ctypes.c_longlong
+    out = {}
+    ws = torch.zeros(1 << 22, dtype=torch.uint8, device="cuda")
+    for lg in (10, 12, 14, 16, 17, 18, 19, 20, 21, 22):
+        n = 1 << lg
+        x = torch.randint(-1000, 1000, (n,), dtype=torch.int32, device="cuda")
+        y = torch.empty_like(x)
+        row = {"product_us": round(graph_per_call(lambda: S.inclusive_scan(x, out=y)), 2)}
+        for v, name in NAMES.items():
+            for coop in (1, 0):
+                tiles = -(-n // L.lab_block_elems(v))
+                if (v in (4, 5) and tiles > 16) or (coop == 0 and tiles <= 16) or tiles > 16 * 14:
+                    continue
+
+                def f(v=v, coop=coop):
+                    rc = L.lab_cluster(v, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), coop,
+                                       torch.cuda.current_stream().cuda_stream)
+                    assert rc == 0, rc
+                key = name + ("" if coop else "_nocoop") + "_us"
+                row[key] = round(graph_per_call(f), 2)
+                if v not in (4, 5):
+                    f()
+                    torch.cuda.synchronize()
+                    assert torch.equal(y, torch.cumsum(x, 0, dtype=torch.int32)), name
+        out[f"2^{lg}"] = row
+        print(f"2^{lg}", json.dumps(row), flush=True)
+    print(json.dumps({"cluster_lab_graph_us_i32": out}))
+
+
+if __name__ == "__main__":
+    main()

@@ -82,12 +82,19 @@ def main():
                     gms = None
                     graph_err = str(e)[:200]
             cub = bench.cub_gelems(tok, x, reps, 3)
+            cub_g = None
+            if not a.no_graph:
+                try:
+                    cub_g = bench.cub_gelems(tok, x, reps, 3, graph=True)
+                except Exception:
+                    cub_g = None
             hbm = 2 * n * es > (256 << 20)
             row = {"dtype": tok, "log2n": lg, "n": n, "ms": round(ms, 5),
                    "gelems": round(n / (ms * 1e-3) * 1e-9, 2),
                    "graph_ms": None if gms is None else round(gms, 5),
                    "graph_gelems": None if gms is None else round(n / (gms * 1e-3) * 1e-9, 2),
                    "cub_gelems": None if cub is None else round(cub, 2),
+                   "cub_graph_gelems": None if cub_g is None else round(cub_g, 2),
                    "frac_of_measured_hbm": round(2 * n * es / (ms * 1e-3) / 1e9 / peak, 4) if hbm else None}
             rows.append(row)
             print(json.dumps(row), flush=True)

@@ -156,3 +156,25 @@ def test_c_demo_runs(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "c_abi_demo ok" in r.stdout
+
+
+def test_every_module_imports():
+    import importlib
+    import pkgutil
+    for m in pkgutil.iter_modules(P.__path__):
+        if m.name == "__main__":
+            continue
+        importlib.import_module(f"paper_1604_04815_b200.{m.name}")
+
+
+def test_torch_api_rejects_host_tensors():
+    """No CPU fallback: host tensors are refused before anything is launched."""
+    import torch
+    from paper_1604_04815_b200 import scan as S
+    x = torch.arange(10, dtype=torch.int32)
+    with pytest.raises(ValueError, match="CUDA"):
+        S.inclusive_scan(x)
+    with pytest.raises(ValueError, match="CUDA"):
+        S.exclusive_scan(x)
+    with pytest.raises(P.ShapeError):
+        S.inclusive_scan(torch.zeros(2, 2, dtype=torch.int32))

@@ -22,8 +22,21 @@ def sha16(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
 
 
+@pytest.fixture(scope="module", params=["auto", "persistent"])
+def S(request):
+    """Every case on the automatic kernel choice (small n -> the one-cluster
+    latency kernel) and again with the persistent chain forced for all n."""
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    from paper_1604_04815_b200 import scan
+    with scan.force_path(request.param):
+        yield scan
+
+
 @pytest.fixture(scope="module")
-def S():
+def S1():
+    """Automatic kernel choice only: for cases whose sizes are all above the
+    cluster kernel's range (both choices would run the same kernel)."""
     if not torch.cuda.is_available():
         pytest.fail("GPU test run without a CUDA device")
     from paper_1604_04815_b200 import scan
@@ -71,13 +84,13 @@ def test_kats(S, golden):
 
 
 @pytest.mark.parametrize("tok", TOKS)
-def test_digest_2p20(S, golden, oracle_lib, tok):
+def test_digest_2p20(S1, golden, oracle_lib, tok):
     case = next(c for c in golden["digests"]["cases"] if c["n"] == 2 ** 20 and c["dtype"] == tok)
     n = case["n"]
     x = oracle_lib.generate_input(n, tok, [0, n])
     assert sha16(x) == case["x_sha16"]
-    y = run(S, x)
-    ye = run(S, x, exclusive=True)
+    y = run(S1, x)
+    ye = run(S1, x, exclusive=True)
     if tok[0] == "i":
         assert sha16(y) == case["y_sha16"]
         assert sha16(ye) == case["excl_sha16"]
@@ -87,14 +100,14 @@ def test_digest_2p20(S, golden, oracle_lib, tok):
 
 
 @pytest.mark.parametrize("tok", TOKS)
-def test_digest_2p28(S, golden, oracle_lib, tok):
+def test_digest_2p28(S1, golden, oracle_lib, tok):
     # BASELINE.json configs[1]/[2]: N = 2^28, the metric's workload
     case = next(c for c in golden["digests"]["cases"] if c["n"] == 2 ** 28 and c["dtype"] == tok)
     n = case["n"]
     x = oracle_lib.generate_input(n, tok, [0, n])
     assert sha16(x) == case["x_sha16"]
     xd = torch.from_numpy(x).cuda()
-    yd = S.inclusive_scan(xd)
+    yd = S1.inclusive_scan(xd)
     y = yd.cpu().numpy()
     if tok[0] == "i":
         assert sha16(y) == case["y_sha16"]
@@ -102,7 +115,7 @@ def test_digest_2p28(S, golden, oracle_lib, tok):
     else:
         check(x, y, oracle_lib, what=tok)
         # deterministic association: a second run is bit-identical
-        y2 = S.inclusive_scan(xd).cpu().numpy()
+        y2 = S1.inclusive_scan(xd).cpu().numpy()
         assert np.array_equal(y.view(np.uint8), y2.view(np.uint8))
 
 
@@ -119,32 +132,32 @@ def test_sizes_around_tiles_and_rounds(S, oracle_lib, tok):
 
 
 @pytest.mark.parametrize("tok", TOKS)
-def test_in_place(S, oracle_lib, tok):
+def test_in_place(S1, oracle_lib, tok):
     n = 1_000_003
     x = oracle_lib.generate_input(n, tok, [7, 77])
     xd = torch.from_numpy(x).cuda()
-    got = S.inclusive_scan(xd, out=xd)
+    got = S1.inclusive_scan(xd, out=xd)
     assert got.data_ptr() == xd.data_ptr()
     check(x, xd.cpu().numpy(), oracle_lib, what="in-place")
     x2 = torch.from_numpy(x).cuda()
-    S.exclusive_scan(x2, out=x2)
+    S1.exclusive_scan(x2, out=x2)
     check(x, x2.cpu().numpy(), oracle_lib, exclusive=True, what="in-place exclusive")
 
 
 @pytest.mark.parametrize("tok", TOKS)
-def test_misaligned_generic_path(S, oracle_lib, tok):
+def test_misaligned_generic_path(S1, oracle_lib, tok):
     # x offset by one element: not 16-byte aligned -> the generic (non-TMA) kernel
     n = 777_777
     x = oracle_lib.generate_input(n + 1, tok, [5, n])
     xd = torch.from_numpy(x).cuda()[1:]
     assert xd.data_ptr() % 16 != 0
-    y = S.inclusive_scan(xd).cpu().numpy()
+    y = S1.inclusive_scan(xd).cpu().numpy()
     check(x[1:].copy(), y, oracle_lib, what="misaligned")
 
 
 @pytest.mark.parametrize("tok", TOKS)
 @pytest.mark.parametrize("shift", [1, 2, 3])
-def test_congruent_misalignment_split_path(S, oracle_lib, tok, shift):
+def test_congruent_misalignment_split_path(S1, oracle_lib, tok, shift):
     # x and y misaligned by the same amount (a slice scanned in place, or two
     # slices at equal offsets): head elements on the generic kernel, the rest
     # on the TMA kernel with the head's total as carry
@@ -158,26 +171,26 @@ def test_congruent_misalignment_split_path(S, oracle_lib, tok, shift):
     assert xd.data_ptr() % 16 != 0
     tot = torch.empty(1, dtype=xd.dtype, device="cuda")
     other = torch.empty(n + shift, dtype=xd.dtype, device="cuda")[shift:]
-    S.inclusive_scan(xd, out=other, total_out=tot)
+    S1.inclusive_scan(xd, out=other, total_out=tot)
     check(x[shift:].copy(), other.cpu().numpy(), oracle_lib, what="split out-of-place")
-    S.exclusive_scan(xd, out=other)
+    S1.exclusive_scan(xd, out=other)
     check(x[shift:].copy(), other.cpu().numpy(), oracle_lib, exclusive=True, what="split exclusive")
-    S.inclusive_scan(xd, out=xd)
+    S1.inclusive_scan(xd, out=xd)
     check(x[shift:].copy(), xd.cpu().numpy(), oracle_lib, what="split in-place")
     if tok[0] == "i":
         assert tot.item() == oracle_lib.c_sequential_scan(x[shift:].copy())[1]
 
 
 @pytest.mark.parametrize("tok", TOKS)
-def test_carry_in_total_out(S, oracle_lib, tok):
+def test_carry_in_total_out(S1, oracle_lib, tok):
     n = 3_000_001
     x = oracle_lib.generate_input(n, tok, [1, 2])
     cut = 1_234_567
     xd = torch.from_numpy(x).cuda()
     t1 = torch.empty(1, dtype=xd.dtype, device="cuda")
     t2 = torch.empty(1, dtype=xd.dtype, device="cuda")
-    y1 = S.inclusive_scan(xd[:cut].clone(), total_out=t1)
-    y2 = S.inclusive_scan(xd[cut:].clone(), carry_in=t1, total_out=t2)
+    y1 = S1.inclusive_scan(xd[:cut].clone(), total_out=t1)
+    y2 = S1.inclusive_scan(xd[cut:].clone(), carry_in=t1, total_out=t2)
     y = torch.cat([y1, y2]).cpu().numpy()
     check(x, y, oracle_lib, what="carry chain")
     ref_total = oracle_lib.c_sequential_scan(x)[1]
@@ -220,11 +233,11 @@ def test_empty(S):
         assert tot.item() == 0
 
 
-def test_float_determinism_across_calls(S, oracle_lib):
+def test_float_determinism_across_calls(S1, oracle_lib):
     for tok in ("f32", "f64"):
         x = oracle_lib.generate_input(5_000_000, tok, [0, 3])
         xd = torch.from_numpy(x).cuda()
-        ys = [S.inclusive_scan(xd).cpu().numpy() for _ in range(3)]
+        ys = [S1.inclusive_scan(xd).cpu().numpy() for _ in range(3)]
         for y in ys[1:]:
             assert np.array_equal(ys[0].view(np.uint8), y.view(np.uint8))
 
@@ -250,7 +263,7 @@ def test_noncontiguous_input_is_made_contiguous(S, oracle_lib):
 
 
 @pytest.mark.slow
-def test_largest_size_checksum(S, oracle_lib):
+def test_largest_size_checksum(S1, oracle_lib):
     # 2^30 i32 (4 GiB): the top of the BASELINE sweep, compared via a digest
     n = 1 << 30
     x = np.empty(n, dtype=np.int32)
@@ -259,5 +272,5 @@ def test_largest_size_checksum(S, oracle_lib):
         x[off:off + part.size] = part
         off += part.size
     ref, _ = oracle_lib.c_sequential_scan(x)
-    y = S.inclusive_scan(torch.from_numpy(x).cuda()).cpu().numpy()
+    y = S1.inclusive_scan(torch.from_numpy(x).cuda()).cpu().numpy()
     assert sha16(y) == sha16(ref)
