@@ -80,6 +80,13 @@ extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n,
     case 43: return run_ws<12, 49152, 3>(x, y, n, ws, s, grid_out);
     case 44: return run_ws<16, 65536, 3>(x, y, n, ws, s, grid_out);
     case 45: return run_ws<4, 32768, 6>(x, y, n, ws, s, grid_out);
+    // mid-n candidates: smaller tiles / fewer stages, several CTAs per SM
+    case 46: return run_ws<8, 16384, 4>(x, y, n, ws, s, grid_out);
+    case 47: return run_ws<4, 16384, 4>(x, y, n, ws, s, grid_out);
+    case 48: return run_ws<8, 16384, 3>(x, y, n, ws, s, grid_out);
+    case 49: return run_ws<4, 8192, 4>(x, y, n, ws, s, grid_out);
+    case 50: return run_ws<8, 32768, 2>(x, y, n, ws, s, grid_out);
+    case 51: return run_ws<4, 16384, 2>(x, y, n, ws, s, grid_out);
     }
     return -3;
 }

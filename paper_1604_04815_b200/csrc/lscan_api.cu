@@ -93,6 +93,16 @@ bool cluster_path_enabled() {
     return on;
 }
 
+// LSCAN_NO_PDL=1: launch the latency kernel without programmatic dependent
+// launch (lab A/B of the overlap between back-to-back calls)
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LSCAN_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 bool valid_dtype(ls_dtype dt) { return dt >= LS_I32 && dt <= LS_F64; }
 bool valid_op(ls_op op) { return op >= LS_OP_ADD && op <= LS_OP_MIN; }
 
@@ -300,11 +310,18 @@ ls_status launch_cluster(const DevState &d, ls_op op, ls_dtype dt, const void *x
     attr[0].val.clusterDim.x = (unsigned)C;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    // several clusters wait on each other's aggregates: all must be resident
-    attr[1].id = cudaLaunchAttributeCooperative;
-    attr[1].val.cooperative = 1;
+    if (clusters > 1) {
+        // several clusters wait on each other's aggregates: all must be resident
+        attr[1].id = cudaLaunchAttributeCooperative;
+        attr[1].val.cooperative = 1;
+    } else {
+        // one cluster: may launch early behind the previous kernel (PDL); the
+        // kernel's griddepcontrol.wait keeps the data dependency
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = clusters > 1 ? 2 : 1;
+    cfg.numAttrs = (clusters > 1 || pdl_enabled()) ? 2 : 1;
     LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "cluster scan kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return LS_OK;

@@ -85,6 +85,13 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     __shared__ T s_pre;                    // carry (+) clusters before this one (+) blocks before this one
     __shared__ int s_has;
 
+    // programmatic dependent launch: the grid may start while the previous
+    // kernel in the stream drains; nothing global is touched before this wait
+    // (which returns once that kernel has completed and flushed), and the
+    // next kernel may begin launching as soon as every block got here
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t r = cluster_ctarank();
     const uint32_t C = cluster_nctarank();

@@ -107,18 +107,34 @@ def _ws_bytes(dt: int, n: int) -> int:
     return b
 
 
+_get_device = getattr(torch._C, "_cuda_getDevice", torch.cuda.current_device)
+
+
 def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exclusive: bool,
           op: str = "add") -> torch.Tensor:
-    _check_1d(x)
-    dt = dtype_code(x.dtype)
-    oc = op_code(op)
+    # the per-call path is kept lean (it is most of the cost of a small scan):
+    # integer device indices, raw stream pointers, cached workspace sizes
+    if type(x) is not torch.Tensor and not isinstance(x, torch.Tensor):
+        raise TypeError("input must be a torch.Tensor")
+    if x.dim() != 1:
+        raise ShapeError(f"input must be 1-D, got shape {tuple(x.shape)}")
+    if not x.is_cuda:
+        raise ValueError("input must be a CUDA tensor (there is no CPU path)")
+    dt = TORCH_DT.get(x.dtype)
+    if dt is None:
+        dtype_code(x.dtype)  # raises UnsupportedOperatorError
+    oc = N.OPS.get(op)
+    if oc is None:
+        op_code(op)  # raises UnsupportedOperatorError
+    idx = x.get_device()
+    n = x.numel()
     if out is None:
         out = torch.empty_like(x, memory_format=torch.contiguous_format)
     elif out is not x:
         _check_1d(out, "out")
-        if out.shape != x.shape:
+        if out.numel() != n:
             raise ShapeError("out shape must match input shape")
-        if out.dtype != x.dtype or out.device != x.device:
+        if out.dtype != x.dtype or out.get_device() != idx:
             raise ValueError("out must have the input's dtype and device")
         if not out.is_contiguous():
             raise ShapeError("out must be contiguous")
@@ -126,20 +142,18 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
         if out is x:
             raise ShapeError("in-place scan needs a contiguous tensor")
         x = x.contiguous()
-    n = x.numel()
-    dev = x.device
-    idx = dev.index
-    switch = idx != torch.cuda.current_device()
+    prev = _get_device()
+    switch = idx != prev
     if switch:
-        prev = torch.cuda.current_device()
         torch.cuda.set_device(idx)
     try:
         sp = _raw_stream(idx)
         ws = _workspaces.get((idx, sp))
         need = _ws_bytes(dt, n)
         if ws is None or ws.numel() < need:
-            ws = workspace(dev, torch.cuda.current_stream(dev), need)
-        fn = N.lib().ls_exclusive_scan if exclusive else N.lib().ls_inclusive_scan
+            ws = workspace(x.device, torch.cuda.current_stream(x.device), need)
+        L = N.lib()
+        fn = L.ls_exclusive_scan if exclusive else L.ls_inclusive_scan
         rc = fn(oc, dt, x.data_ptr() if n else None, out.data_ptr() if n else None, n,
                 None if carry_in is None else _scalar_ptr(carry_in, x, "carry_in"),
                 None if total_out is None else _scalar_ptr(total_out, x, "total_out"),

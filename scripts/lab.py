@@ -22,7 +22,9 @@ from paper_1604_04815_b200 import _native as N  # noqa: E402
 # scanner warps / tile bytes / stages (bench_support/lscan_lab.cu)
 CFG_NAMES = {30: "reg16/32K/4", 31: "reg16/32K/5", 32: "reg16/32K/6", 33: "reg16/32K/7", 34: "reg8/32K/6",
              35: "reg16/64K/3", 36: "reg16/16K/12", 37: "reg8/16K/12", 38: "reg24/48K/4", 40: "reg12/48K/4",
-             41: "reg8/32K/5", 42: "reg8/32K/4", 43: "reg12/48K/3", 44: "reg16/64K/3", 45: "reg4/32K/6"}
+             41: "reg8/32K/5", 42: "reg8/32K/4", 43: "reg12/48K/3", 44: "reg16/64K/3", 45: "reg4/32K/6",
+             46: "reg8/16K/4", 47: "reg4/16K/4", 48: "reg8/16K/3", 49: "reg4/8K/4", 50: "reg8/32K/2",
+             51: "reg4/16K/2"}
 
 
 def timeit(fn, reps, warm=3):
@@ -38,6 +40,22 @@ def timeit(fn, reps, warm=3):
     return a.elapsed_time(b) / reps
 
 
+def graph_ms(fn, reps):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    return timeit(g.replay, 3, warm=1) / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=1 << 28)
@@ -46,6 +64,8 @@ def main():
     ap.add_argument("--wide", action="store_true", help="64-bit elements (same as --dtype i64)")
     ap.add_argument("--dtype", choices=["i32", "i64", "f32", "f64"], default=None)
     ap.add_argument("--labso", default="liblscanlab.so", help="lab library in bench_support/_build")
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (device time, no host)")
+    ap.add_argument("--product", action="store_true", help="also time the product call (scan.inclusive_scan)")
     args = ap.parse_args()
     L = N.lib()
     LAB = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", args.labso))
@@ -63,7 +83,6 @@ def main():
         x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda")
     y = torch.empty_like(x)
     ws = torch.zeros(L.ls_workspace_bytes(N.LS_I64, n) * 8, dtype=torch.uint8, device="cuda")
-    s = torch.cuda.current_stream().cuda_stream
     g = ctypes.c_int64(0)
     ref = torch.cumsum(x, 0, dtype=dt) if not dt.is_floating_point else torch.cumsum(x.double(), 0)
     res = {"n": n, "dtype": str(dt), "lib": args.labso}
@@ -72,16 +91,23 @@ def main():
                                                    args.reps) * 1e-3) * 1e-9, 1)
     for cfg in [int(c) for c in args.cfgs.split(",")]:
         def step():
-            rc = LAB.ls_lab_run(cfg, code << 8, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), s,
-                                ctypes.byref(g))
+            rc = LAB.ls_lab_run(cfg, code << 8, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream, ctypes.byref(g))
             assert rc == 0, rc
-        ms = timeit(step, args.reps)
+        ms = graph_ms(step, args.reps) if args.graph else timeit(step, args.reps)
         res[f"cfg{cfg}_{CFG_NAMES[cfg]}"] = {
             "gelems": round(n / (ms * 1e-3) * 1e-9, 1), "gbs": round(2 * n * es / (ms * 1e-3) / 1e9, 1),
             "grid": g.value,
             "ok": bool(torch.equal(y, ref)) if not dt.is_floating_point
             else bool(((y.double() - ref).abs() <= 1e-4 * torch.cumsum(x.double().abs(), 0)).all())}
-    print(json.dumps(res, indent=1))
+    if args.product:
+        from paper_1604_04815_b200 import scan as S
+
+        def prod():
+            S.inclusive_scan(x, out=y)
+        ms = graph_ms(prod, args.reps) if args.graph else timeit(prod, args.reps)
+        res["product"] = {"gelems": round(n / (ms * 1e-3) * 1e-9, 1), "us": round(ms * 1e3, 2)}
+    print(json.dumps(res, indent=None if args.graph else 1))
 
 
 if __name__ == "__main__":

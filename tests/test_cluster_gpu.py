@@ -161,3 +161,43 @@ def test_graph_capture_replay(S, oracle_lib):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(yd.cpu().numpy(), oracle_lib.sequential_scan(x2))
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_dependent_chain(S, oracle_lib, graph):
+    """Back-to-back scans where each reads the previous one's output (the
+    programmatic-dependent-launch overlap must keep the data dependency),
+    with a torch kernel in between every few calls; eager and graph-replayed."""
+    n = 30_001
+    x0 = oracle_lib.generate_input(n, "i32", [8, 8])
+    bufs = [torch.from_numpy(x0).cuda()] + [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(12)]
+
+    def chain():
+        for i in range(12):
+            S.inclusive_scan(bufs[i], out=bufs[i + 1])
+            if i % 4 == 3:
+                bufs[i + 1].add_(1)
+
+    if graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            chain()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                chain()
+        torch.cuda.synchronize()
+        for b in bufs[1:]:
+            b.zero_()
+        g.replay()
+    else:
+        chain()
+    torch.cuda.synchronize()
+    want = x0
+    with np.errstate(over="ignore"):
+        for i in range(12):
+            want = oracle_lib.sequential_scan(want)
+            if i % 4 == 3:
+                want = (want + np.int32(1)).astype(np.int32)
+    assert np.array_equal(bufs[-1].cpu().numpy(), want)
