@@ -7,6 +7,8 @@
 //     0: 256 threads, 4 rows (product)    1: 512 threads, 4 rows
 //     2: 256 threads, 8 rows              3: 256 threads, 2 rows
 //     4: copy 1024 x 4 rows               5: copy 256 x 4 rows
+//     6: 256 x 16 rows (2 blocks/SM)       7: 256 x 8 rows (2 blocks/SM, product mid)
+//     8: int64 256 x 4 (product small)     9: int64 256 x 8 (product mid)
 //   lab_block_elems(variant) -> elements per block (int32)
 #include <cuda_runtime.h>
 
@@ -40,6 +42,7 @@ struct Var {
     void (*fn)(const ScanParams);
     int threads;
     int rows;
+    int es = 4;  // element size
 };
 Var var(int v) {
     switch (v) {
@@ -50,7 +53,10 @@ Var var(int v) {
     case 4: return {&copy_kernel<1024, 4>, 1024, 4};
     case 5: return {&copy_kernel<256, 4>, 256, 4};
     case 6: return {&scan_cluster_kernel<int32_t, OpAdd, false, 16, 256, 2>, 256, 16};
-    default: return {&scan_cluster_kernel<int32_t, OpAdd, false, 8, 256, 2>, 256, 8};
+    case 7: return {&scan_cluster_kernel<int32_t, OpAdd, false, 8, 256, 2>, 256, 8};
+    // 64-bit elements, small and mid geometry
+    case 8: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 256, 4>, 256, 4, 8};
+    default: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 256, 2>, 256, 8, 8};
     }
 }
 }  // namespace
@@ -58,7 +64,7 @@ Var var(int v) {
 extern "C" {
 long long lab_block_elems(int v) {
     const Var w = var(v);
-    return (long long)w.threads * w.rows * 4;
+    return (long long)w.threads * w.rows * 16 / w.es;
 }
 
 // ws: a zeroed workspace (needed when n spans several clusters); coop: 0
@@ -70,7 +76,7 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     const int C = (int)(tiles < 16 ? tiles : 16);
     const long long K = (tiles + C - 1) / C;
     if (C < 1 || (K > 1 && ((v == 4 || v == 5) || !ws))) return -1;
-    static bool init[8] = {};
+    static bool init[16] = {};
     if (!init[v]) {
         cudaFuncSetAttribute((const void *)w.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         init[v] = true;

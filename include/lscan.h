@@ -191,11 +191,12 @@ ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]);
  * blocks per cluster (0 = unavailable), out[1] = elements per block (one
  * tile each) while n fits one cluster, out[2] = co-resident clusters of the
  * mid geometry, out[3] = largest n the kernel takes, out[4] = elements per
- * block of the mid geometry.  A scan of n <= out[3] elements (debug hooks
- * disarmed) is one launch: carries travel through distributed shared memory
- * inside a cluster and through epoch-tagged workspace slots between
+ * block of the mid geometry, out[5] = largest n on mid tiles (beyond it,
+ * tiles of 3 * out[1] elements).  A scan of n <= out[3] elements (debug
+ * hooks disarmed) is one launch: carries travel through distributed shared
+ * memory inside a cluster and through epoch-tagged workspace slots between
  * clusters. */
-ls_status ls_query_cluster(ls_dtype dt, int64_t out[5]);
+ls_status ls_query_cluster(ls_dtype dt, int64_t out[6]);
 /* Number of kernel launches this process has issued through the library. */
 int64_t ls_launch_count(void);
 

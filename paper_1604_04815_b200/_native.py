@@ -142,7 +142,7 @@ def lib():
             "ls_ipc_close": (ci, [vp]),
             "ls_debug_slot_stress": (ci, [ci, i64, ci, ctypes.POINTER(ctypes.c_int64)]),
             "ls_debug_force_path": (ci, [ci]),
-            "ls_query_cluster": (ci, [ci, ctypes.POINTER(ctypes.c_int64)]),  # out[5]
+            "ls_query_cluster": (ci, [ci, ctypes.POINTER(ctypes.c_int64)]),  # out[6]
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

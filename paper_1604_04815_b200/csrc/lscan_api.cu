@@ -140,7 +140,7 @@ struct DevState {
     int occ_multi[4][kNumOps][2] = {};
     int reduce_occ[4][kNumOps] = {};
     int cluster_max = 0;          // largest schedulable cluster of the latency kernel (0: path off)
-    int cluster_capacity[2] = {};  // co-resident clusters of that size [small, mid] (min over instances)
+    int cluster_capacity[kClusterGeoms] = {};  // co-resident clusters of that size per geometry (min over instances)
 };
 std::mutex g_dev_mu;
 std::vector<DevState> g_dev;
@@ -185,7 +185,7 @@ ls_status device_state(DevState **out) {
                         "occupancy");
                 d.reduce_occ[dt][op] = std::max(occ, 1);
                 for (int ex = 0; ex < 2; ++ex)
-                    for (int g = 0; g < 2; ++g)
+                    for (int g = 0; g < kClusterGeoms; ++g)
                         LS_CUDA(cudaFuncSetAttribute((const void *)k.cluster[op][ex][g].fn,
                                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                                 "cudaFuncSetAttribute(non-portable cluster size)");
@@ -196,8 +196,9 @@ ls_status device_state(DevState **out) {
         // how many fit at once (the minimum over every instance)
         d.cluster_max = 0;
         for (int c : {kClusterMax, 8}) {
-            int cap[2] = {1 << 30, 1 << 30};
-            for (int g = 0; g < 2; ++g)
+            int cap[kClusterGeoms];
+            for (int g = 0; g < kClusterGeoms; ++g) cap[g] = 1 << 30;
+            for (int g = 0; g < kClusterGeoms; ++g)
                 for (int dt = 0; dt < 4; ++dt)
                     for (int op = 0; op < kNumOps; ++op)
                         for (int ex = 0; ex < 2; ++ex) {
@@ -219,10 +220,9 @@ ls_status device_state(DevState **out) {
                             }
                             cap[g] = std::min(cap[g], nc);
                         }
-            if (cap[0] >= 1 && cap[1] >= 1) {
+            if (cap[0] >= 1 && cap[1] >= 1 && cap[2] >= 1) {
                 d.cluster_max = c;
-                d.cluster_capacity[0] = cap[0];
-                d.cluster_capacity[1] = cap[1];
+                for (int g = 0; g < kClusterGeoms; ++g) d.cluster_capacity[g] = cap[g];
                 break;
             }
         }
@@ -279,10 +279,16 @@ ls_status identity_fill(ls_op op, ls_dtype dt, void *dst, const void *carry_in, 
 // Small and mid n: one tile per block, clusters of up to d.cluster_max
 // blocks (carries through DSMEM), several clusters co-resident by a
 // cooperative launch (cluster aggregates through epoch-tagged slots).
-// Geometry g: 0 = small tiles (n fits one cluster of them), 1 = mid tiles.
+// Geometry g: 0 = small tiles (n fits one cluster of them), 1 = mid tiles
+// (while their clusters fit at once), 2 = large tiles.
+int64_t cluster_span(const DevState &d, ls_dtype dt, int g) {  // elements the geometry covers
+    const int64_t te = K(dt).cluster[0][0][g].tile_bytes / elem_size(dt);
+    return te * d.cluster_max * (g == 0 ? 1 : d.cluster_capacity[g]);
+}
+
 int cluster_geometry(const DevState &d, ls_dtype dt, int64_t n) {
-    const int64_t te = K(dt).cluster[0][0][0].tile_bytes / elem_size(dt);
-    return n <= te * d.cluster_max ? 0 : 1;
+    if (n <= cluster_span(d, dt, 0)) return 0;
+    return n <= cluster_span(d, dt, 1) ? 1 : 2;
 }
 
 ls_status launch_cluster(const DevState &d, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
@@ -328,17 +334,16 @@ ls_status launch_cluster(const DevState &d, ls_op op, ls_dtype dt, const void *x
 }
 
 // largest n the cluster kernel takes: one cluster of small tiles always;
-// mid tiles up to the co-resident capacity and the measured crossover with
-// the persistent kernel (LSCAN_CLUSTER_MAX_BYTES overrides it for labs)
+// mid / large tiles up to their co-resident capacity and the measured
+// crossover with the persistent kernel (LSCAN_CLUSTER_MAX_BYTES overrides it
+// for labs)
 int64_t cluster_limit(const DevState &d, ls_dtype dt) {
     static const int64_t max_bytes = [] {
         const char *e = getenv("LSCAN_CLUSTER_MAX_BYTES");
         return e ? std::max<int64_t>(0, atoll(e)) : kClusterMaxBytes;
     }();
-    const int64_t es = elem_size(dt);
-    const int64_t one_small = K(dt).cluster[0][0][0].tile_bytes / es * d.cluster_max;
-    const int64_t coresident = K(dt).cluster[0][0][1].tile_bytes / es * d.cluster_max * d.cluster_capacity[1];
-    return std::max(one_small, std::min(coresident, max_bytes / es));
+    const int64_t coresident = std::max(cluster_span(d, dt, 1), cluster_span(d, dt, 2));
+    return std::max(cluster_span(d, dt, 0), std::min(coresident, max_bytes / elem_size(dt)));
 }
 
 bool use_cluster(const DevState &d, ls_dtype dt, int64_t n, const DebugCfg &dbg) {
@@ -731,7 +736,7 @@ ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]) {
     return LS_OK;
 }
 
-ls_status ls_query_cluster(ls_dtype dt, int64_t out[5]) {
+ls_status ls_query_cluster(ls_dtype dt, int64_t out[6]) {
     if (!valid_dtype(dt) || !out) return fail(LS_ERR_INVALID_ARG, "bad arguments");
     DevState *d = nullptr;
     ls_status st = device_state(&d);
@@ -741,6 +746,7 @@ ls_status ls_query_cluster(ls_dtype dt, int64_t out[5]) {
     out[2] = cluster_path_enabled() ? d->cluster_capacity[1] : 0;
     out[3] = cluster_path_enabled() ? cluster_limit(*d, dt) : 0;
     out[4] = K(dt).cluster[0][0][1].tile_bytes / elem_size(dt);
+    out[5] = cluster_path_enabled() ? cluster_span(*d, dt, 1) : 0;
     return LS_OK;
 }
 

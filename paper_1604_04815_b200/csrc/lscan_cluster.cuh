@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
 
     __shared__ T warp_tot[WARPS];
     __shared__ T warp_exc[WARPS];
+    __shared__ T row_tot[WARPS][V];       // per warp: totals of its rows
     __shared__ Bits cta_agg[kClusterMax];  // aggregates of the lower blocks of this cluster, stored by them
     __shared__ T block_agg;
     __shared__ T s_pre;                    // carry (+) clusters before this one (+) blocks before this one
@@ -108,21 +109,31 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     Header *hdr = reinterpret_cast<Header *>(p.ws);
     const uint32_t tag = K > 1 ? call_tag(hdr) : 0u;
 
-    // ---- load: row j of warp w is vectors w*WARP_VECS + j*32 + lane
+    // ---- load: row j of warp w is vectors w*WARP_VECS + j*32 + lane.
+    //      Whole aligned tiles take a branch-free path so all V loads are in
+    //      flight at once (a per-row branch makes the compiler wait on each).
     Regs<T, V> d;
+    if (xv && valid == TILE_ELEMS) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-        const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
-        if (xv && e0 + PER <= valid) {
-            d.q[j] = ldg128(x + e0);
-        } else {
+        for (int j = 0; j < V; ++j) d.q[j] = ldg128(x + (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER);
+    } else {
 #pragma unroll
-            for (int e = 0; e < PER; ++e) d.e[j * PER + e] = e0 + e < valid ? x[e0 + e] : ident;
+        for (int j = 0; j < V; ++j) {
+            const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
+            if (xv && e0 + PER <= valid) {
+                d.q[j] = ldg128(x + e0);
+            } else {
+#pragma unroll
+                for (int e = 0; e < PER; ++e) d.e[j * PER + e] = e0 + e < valid ? x[e0 + e] : ident;
+            }
         }
     }
 
-    // ---- per row: lane-serial fold of the vector, inclusive warp scan
-    T rex[V], rtot[V];
+    // ---- per row: lane-serial fold of the vector and an inclusive warp scan,
+    //      then the serial row carry (Alg. 2)
+    //      (row totals go to shared memory: registers are kept for the tile)
+    T rex[V];
+    T run = ident;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
         T v = d.e[j * PER];
@@ -130,15 +141,9 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
         for (int e = 1; e < PER; ++e) v = OP::apply(v, d.e[j * PER + e]);
         const T inc = warp_inclusive_scan<T, OP>(v, lane);
         rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
-        rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
-    }
-    T rowpre[V];
-    T run = rtot[0];
-    rowpre[0] = ident;
-#pragma unroll
-    for (int j = 1; j < V; ++j) {
-        rowpre[j] = run;
-        run = OP::apply(run, rtot[j]);
+        const T rt = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) row_tot[warp][j] = rt;
+        run = j == 0 ? rt : OP::apply(run, rt);
     }
     if (lane == 0) warp_tot[warp] = run;
     __syncthreads();
@@ -218,12 +223,18 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
         has0 = true;
     }
 
-    // ---- fold the carry in registers, store
+    // ---- fold the carry in registers, store; rowpre = rows before j (the
+    //      serial row carry, rebuilt here to keep registers for large tiles)
+    T rowpre = row_tot[warp][0];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
         bool has = has0;
         T acc = pre;
-        if (j > 0) { acc = has ? OP::apply(acc, rowpre[j]) : rowpre[j]; has = true; }
+        if (j > 0) {
+            acc = has ? OP::apply(acc, rowpre) : rowpre;
+            has = true;
+            if (j + 1 < V) rowpre = OP::apply(rowpre, row_tot[warp][j]);
+        }
         if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
 #pragma unroll
         for (int e = 0; e < PER; ++e) {
@@ -237,13 +248,21 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
                 d.e[j * PER + e] = acc;
             }
         }
-        const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
-        if (yv && e0 + PER <= valid) {
-            stg128_v4(y + e0, d.q[j]);
-        } else {
+    }
+    if (yv && valid == TILE_ELEMS) {
 #pragma unroll
-            for (int e = 0; e < PER; ++e)
-                if (e0 + e < valid) y[e0 + e] = d.e[j * PER + e];
+        for (int j = 0; j < V; ++j) stg128_v4(y + (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER, d.q[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
+            if (yv && e0 + PER <= valid) {
+                stg128_v4(y + e0, d.q[j]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < PER; ++e)
+                    if (e0 + e < valid) y[e0 + e] = d.e[j * PER + e];
+            }
         }
     }
     // the last block to finish records this call's tag as the workspace epoch

@@ -118,14 +118,17 @@ static_assert(sizeof(Header) == 128, "header is one 128-byte line");
 constexpr int kMaxGrid = 4096;
 
 // the latency kernel (lscan_cluster.cuh): 256-thread blocks, one tile each,
-// in two geometries chosen from the lab (profiles/r1_cluster_lab.json):
+// in three geometries chosen from the lab (profiles/r1_cluster_lab.log):
 //   small: 4 rows of 16-byte vectors per thread (16 KiB tiles), one cluster
 //   mid:   8 rows (32 KiB tiles), several co-resident clusters
+//   large: 12 rows (48 KiB tiles), when the mid tiles no longer fit at once
 constexpr int kClusterThreads = 256;
+constexpr int kClusterGeoms = 3;
 constexpr int kClusterRowsSmall = 4, kClusterMinBlocksSmall = 4;
 constexpr int kClusterRowsMid = 8, kClusterMinBlocksMid = 2;
+constexpr int kClusterRowsLarge = 12, kClusterMinBlocksLarge = 2;
 constexpr int kClusterMax = 16;  // blocks per cluster (non-portable size; 8 where 16 cannot be scheduled)
-constexpr int64_t kClusterMaxBytes = 8ll << 20;  // crossover to the persistent kernel (lab-measured)
+constexpr int64_t kClusterMaxBytes = 16ll << 20;  // crossover to the persistent kernel (lab-measured)
 constexpr size_t kSlotBase = sizeof(Header) + (size_t)kMaxGrid * 8;
 
 struct ScanParams {

@@ -41,6 +41,8 @@ void fill_op(DtypeKernels &k) {
     k.cluster[OP::code][1][0] = cluster_launch<T, OP, true, kClusterRowsSmall, kClusterMinBlocksSmall>();
     k.cluster[OP::code][0][1] = cluster_launch<T, OP, false, kClusterRowsMid, kClusterMinBlocksMid>();
     k.cluster[OP::code][1][1] = cluster_launch<T, OP, true, kClusterRowsMid, kClusterMinBlocksMid>();
+    k.cluster[OP::code][0][2] = cluster_launch<T, OP, false, kClusterRowsLarge, kClusterMinBlocksLarge>();
+    k.cluster[OP::code][1][2] = cluster_launch<T, OP, true, kClusterRowsLarge, kClusterMinBlocksLarge>();
     k.scan[OP::code][0][1] = fast_launch<T, OP, false>();
     k.scan[OP::code][1][1] = fast_launch<T, OP, true>();
     k.scan[OP::code][0][0] = generic_launch<T, OP, false>();

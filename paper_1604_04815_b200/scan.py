@@ -240,11 +240,11 @@ def query_cluster(dtype: torch.dtype) -> dict:
     it takes (``max_elems``) and the largest single-cluster n
     (``one_cluster_elems``)."""
     import ctypes
-    out = (ctypes.c_int64 * 5)()
+    out = (ctypes.c_int64 * 6)()
     raise_for_status(N.lib().ls_query_cluster(dtype_code(dtype), out))
     return {"max_blocks": int(out[0]), "block_elems": int(out[1]), "capacity": int(out[2]),
             "max_elems": int(out[3]), "one_cluster_elems": int(out[0]) * int(out[1]),
-            "mid_block_elems": int(out[4])}
+            "mid_block_elems": int(out[4]), "mid_max_elems": int(out[5])}
 
 
 class force_path:

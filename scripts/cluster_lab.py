@@ -16,7 +16,8 @@ from overhead_lab import graph_per_call  # noqa: E402
 from paper_1604_04815_b200 import scan as S  # noqa: E402
 
 NAMES = {0: "scan_256x4", 1: "scan_512x4", 2: "scan_256x8", 3: "scan_256x2", 4: "copy_1024x4", 5: "copy_256x4",
-         6: "scan_256x16_minb2", 7: "scan_256x8_minb2"}
+         6: "scan_256x16_minb2", 7: "scan_256x8_minb2", 8: "i64_256x4", 9: "i64_256x8_minb2"}
+WIDE = {8, 9}
 
 
 def main():
@@ -28,16 +29,20 @@ def main():
     ws = torch.zeros(1 << 22, dtype=torch.uint8, device="cuda")
     for lg in (10, 12, 14, 16, 17, 18, 19, 20, 21, 22):
         n = 1 << lg
-        x = torch.randint(-1000, 1000, (n,), dtype=torch.int32, device="cuda")
-        y = torch.empty_like(x)
-        row = {"product_us": round(graph_per_call(lambda: S.inclusive_scan(x, out=y)), 2)}
+        x32 = torch.randint(-1000, 1000, (n,), dtype=torch.int32, device="cuda")
+        x64 = x32.long()
+        y32, y64 = torch.empty_like(x32), torch.empty_like(x64)
+        x, y = x32, y32
+        row = {"product_us": round(graph_per_call(lambda: S.inclusive_scan(x32, out=y32)), 2),
+               "product_i64_us": round(graph_per_call(lambda: S.inclusive_scan(x64, out=y64)), 2)}
         for v, name in NAMES.items():
-            for coop in (1, 0):
+            x, y = (x64, y64) if v in WIDE else (x32, y32)
+            for coop in (1,):
                 tiles = -(-n // L.lab_block_elems(v))
                 if (v in (4, 5) and tiles > 16) or (coop == 0 and tiles <= 16) or tiles > 16 * 14:
                     continue
 
-                def f(v=v, coop=coop):
+                def f(v=v, coop=coop, x=x, y=y):
                     rc = L.lab_cluster(v, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(), coop,
                                        torch.cuda.current_stream().cuda_stream)
                     assert rc == 0, rc
@@ -46,10 +51,10 @@ def main():
                 if v not in (4, 5):
                     f()
                     torch.cuda.synchronize()
-                    assert torch.equal(y, torch.cumsum(x, 0, dtype=torch.int32)), name
+                    assert torch.equal(y, torch.cumsum(x, 0, dtype=x.dtype)), name
         out[f"2^{lg}"] = row
         print(f"2^{lg}", json.dumps(row), flush=True)
-    print(json.dumps({"cluster_lab_graph_us_i32": out}))
+    print(json.dumps({"cluster_lab_graph_us": out}))
 
 
 if __name__ == "__main__":

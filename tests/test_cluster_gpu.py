@@ -40,8 +40,10 @@ def sizes(S, tok):
     c = S.query_cluster(TDT[tok])
     B, one, top, Bm = c["block_elems"], c["one_cluster_elems"], c["max_elems"], c["mid_block_elems"]
     Cm = c["max_blocks"] * Bm  # one cluster of mid tiles
+    mid = c["mid_max_elems"]    # beyond: large tiles
     return sorted({1, 2, 3, 5, 31, 32, 33, 1000, 1024, 4097, B - 1, B, B + 1, 2 * B + 7, 5 * B - 3,
-                   one - 1, one, one + 1, Cm - 1, Cm, Cm + 1, 2 * Cm + Bm + 3, top - Bm + 1, top - 1, top})
+                   one - 1, one, one + 1, Cm - 1, Cm, Cm + 1, 2 * Cm + Bm + 3, mid - 1, mid, mid + 1,
+                   top - 3 * B + 1, top - 1, top})
 
 
 def test_cluster_geometry(S):
@@ -67,7 +69,7 @@ def test_cluster_kernel_parity(S, oracle_lib, tok, op):
 
 
 @pytest.mark.parametrize("tok", TOKS)
-@pytest.mark.parametrize("which", ["one_cluster_elems", "max_elems"])
+@pytest.mark.parametrize("which", ["one_cluster_elems", "mid_max_elems", "max_elems"])
 def test_cluster_matches_persistent_kernel(S, oracle_lib, tok, which):
     """Same input through both kernels: ints and max/min bit-identical."""
     n = S.query_cluster(TDT[tok])[which] - 12345
