@@ -30,6 +30,23 @@
 #pragma once
 #include "lscan_common.cuh"
 
+// lab knobs (bench_support/lscan_lab.cu builds; the product uses the defaults):
+// look-back poll back-off, the L2 policy of the TMA loads, and timing-only
+// switches that skip the reducer's pass over the stage / the scanners' row
+// warp scans (wrong sums; they locate the power the kernel draws)
+#ifndef LS_LOOKBACK_SLEEP_NS
+#define LS_LOOKBACK_SLEEP_NS 32
+#endif
+#ifndef LS_TMA_EVICT_FIRST
+#define LS_TMA_EVICT_FIRST 1
+#endif
+#ifndef LS_LAB_SKIP_REDUCE
+#define LS_LAB_SKIP_REDUCE 0
+#endif
+#ifndef LS_LAB_SKIP_ROWSCAN
+#define LS_LAB_SKIP_ROWSCAN 0
+#endif
+
 namespace lscan {
 
 __device__ __forceinline__ void stg128(void *p, uint4 v) {
@@ -117,7 +134,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
                     if (need[u]) { val[u] = ident; need[u] = false; }
                 break;
             }
-            __nanosleep(32);
+            __nanosleep(LS_LOOKBACK_SLEEP_NS);
             if (r_pending) S::load(rnd, r_idx, rw);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -204,7 +221,7 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
 
     if (warp == W_PROD) {
         // ------------------------------------------------------------ producer
-        const uint64_t pol = policy_evict_first();
+        const uint64_t pol = LS_TMA_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
         auto load_tile = [&](int64_t k) {
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
@@ -257,7 +274,7 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int64_t t = c + k * G;
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
             if (p.delay_red_ns > 0 && t % 3 == 1) debug_sleep(p.delay_red_ns);
-            const T a = reduce_stage<T, OP, TILE_BYTES>(stages + s * TILE_BYTES, lane);
+            const T a = LS_LAB_SKIP_REDUCE ? ident : reduce_stage<T, OP, TILE_BYTES>(stages + s * TILE_BYTES, lane);
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&empty[s]);
@@ -401,6 +418,11 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                 T v = r.e[j * PER];
 #pragma unroll
                 for (int e = 1; e < PER; ++e) v = OP::apply(v, r.e[j * PER + e]);
+                if (LS_LAB_SKIP_ROWSCAN) {
+                    rex[j] = v;
+                    rtot[j] = v;
+                    continue;
+                }
                 const T inc = warp_inclusive_scan<T, OP>(v, lane);
                 rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
                 rtot[j] = __shfl_sync(0xffffffffu, inc, 31);

@@ -40,6 +40,19 @@ def timeit(fn, reps, warm=3):
     return a.elapsed_time(b) / reps
 
 
+def effective_sm_mhz():
+    """SM clock actually running (clock64 cycles over globaltimer ns, median
+    over 296 blocks; bench_support/clock_probe.cu) — NVML does not report
+    the sustained-load slowdown."""
+    P = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", "libclockprobe.so"))
+    P.clock_probe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p]
+    buf = torch.zeros(3 * 296, dtype=torch.int64, device="cuda")
+    P.clock_probe(buf.data_ptr(), 296, 200_000, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    v = buf.view(-1, 3).cpu()
+    return round((v[:, 1].double() / v[:, 2].double() * 1e3).median().item(), 1)
+
+
 def graph_ms(fn, reps):
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -66,6 +79,8 @@ def main():
     ap.add_argument("--labso", default="liblscanlab.so", help="lab library in bench_support/_build")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (device time, no host)")
     ap.add_argument("--product", action="store_true", help="also time the product call (scan.inclusive_scan)")
+    ap.add_argument("--sustain", type=int, default=0,
+                    help="report this many consecutive blocks of --reps calls per config (drift under load)")
     args = ap.parse_args()
     L = N.lib()
     LAB = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", args.labso))
@@ -94,6 +109,13 @@ def main():
             rc = LAB.ls_lab_run(cfg, code << 8, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(),
                                 torch.cuda.current_stream().cuda_stream, ctypes.byref(g))
             assert rc == 0, rc
+        if args.sustain:
+            import time
+            time.sleep(3)
+            blocks = [timeit(step, args.reps, warm=0) for _ in range(args.sustain)]
+            res[f"cfg{cfg}_{CFG_NAMES[cfg]}_sustained_gelems"] = [round(n / (b * 1e-3) * 1e-9, 1) for b in blocks]
+            res[f"cfg{cfg}_sm_mhz_after"] = effective_sm_mhz()
+            continue
         ms = graph_ms(step, args.reps) if args.graph else timeit(step, args.reps)
         res[f"cfg{cfg}_{CFG_NAMES[cfg]}"] = {
             "gelems": round(n / (ms * 1e-3) * 1e-9, 1), "gbs": round(2 * n * es / (ms * 1e-3) / 1e9, 1),
