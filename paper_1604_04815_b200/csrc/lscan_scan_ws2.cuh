@@ -46,6 +46,9 @@
 #ifndef LS_LAB_SKIP_ROWSCAN
 #define LS_LAB_SKIP_ROWSCAN 0
 #endif
+#ifndef LS_LAB_SKIP_LOOKBACK
+#define LS_LAB_SKIP_LOOKBACK 0
+#endif
 
 namespace lscan {
 
@@ -313,8 +316,10 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                 // R[k-1]: the caller's carry in round 0, the chain owner's register,
                 // or the published round slot for everyone else
                 const bool need_r = k > 0 && c != G - 1;
-                const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, k - 1, chain, tag, lane,
-                                                              p.spin_budget, hdr, (uint32_t)t);
+                const LookbackOut<T> lb =
+                    LS_LAB_SKIP_LOOKBACK ? LookbackOut<T>{ident, ident, ident}
+                                         : aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, k - 1, chain, tag, lane,
+                                                               p.spin_budget, hdr, (uint32_t)t);
                 T base;
                 if (k == 0) { has = have_carry; base = r_prev; }
                 else if (c == G - 1) { has = true; base = r_prev; }
