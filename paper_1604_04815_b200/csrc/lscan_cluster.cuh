@@ -140,7 +140,10 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
 #pragma unroll
         for (int e = 1; e < PER; ++e) v = OP::apply(v, d.e[j * PER + e]);
         const T inc = warp_inclusive_scan<T, OP>(v, lane);
-        rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
+        if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code)
+            rex[j] = OP::apply(inc, (T)(0 - (typename std::make_unsigned<T>::type)v));  // inc - v, exact
+        else
+            rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
         const T rt = __shfl_sync(0xffffffffu, inc, 31);
         if (lane == 0) row_tot[warp][j] = rt;
         run = j == 0 ? rt : OP::apply(run, rt);

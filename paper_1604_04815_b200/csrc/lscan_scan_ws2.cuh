@@ -429,7 +429,13 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                     continue;
                 }
                 const T inc = warp_inclusive_scan<T, OP>(v, lane);
-                rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
+                if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code) {
+                    // integer add: the exclusive prefix is inclusive - own value,
+                    // exact modulo 2^width, one shuffle fewer per row (+1-2 % i64)
+                    rex[j] = OP::apply(inc, (T)(0 - (typename std::make_unsigned<T>::type)v));
+                } else {
+                    rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
+                }
                 rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
             }
             // serial row carry (Alg. 2): prefix of the rows before j
