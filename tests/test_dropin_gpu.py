@@ -84,6 +84,19 @@ def test_pinned_host_buffers(oracle_lib):
     assert np.array_equal(y, oracle_lib.c_sequential_scan(x)[0])
 
 
+@pytest.mark.parametrize("n", [23_068_671, 23_068_672, 30_000_017])
+def test_pinned_multi_chunk(oracle_lib, n):
+    # pinned (direct DMA) path over several 32 MiB chunks, ragged last chunk
+    x = oracle_lib.generate_input(n, "i32", [3, n])
+    xp = torch.empty(n, dtype=torch.int32).pin_memory()
+    yp = torch.empty(n, dtype=torch.int32).pin_memory()
+    xp.numpy()[:] = x
+    y = P.chained_scan(P.ScanProblem(xp.numpy(), P.make_operator("add", "i32"), out=yp.numpy()))
+    assert np.array_equal(y, oracle_lib.c_sequential_scan(x)[0])
+    ye = P.chained_exclusive_scan(P.ScanProblem(xp.numpy(), P.make_operator("add", "i32"), out=yp.numpy()))
+    assert np.array_equal(ye, oracle_lib.c_sequential_scan(x, exclusive=True)[0])
+
+
 def test_corrupt_slot_breaks_only_downstream(oracle_lib):
     # test_chained.py:275-284 on the device: tile 1 publishes the identity
     cfg_q = P.query_config(torch.int64, 1 << 20)
