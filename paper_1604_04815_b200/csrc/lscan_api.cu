@@ -388,12 +388,20 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     cfg.blockDim = dim3((unsigned)L.threads);
     cfg.dynamicSmemBytes = L.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (cooperative_launch()) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na++].val.cooperative = 1;
+    }
+    if (fast && pdl_enabled()) {
+        // the TMA kernel waits on griddepcontrol before touching global
+        // memory, so it may launch behind the previous kernel's tail
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cfg.numAttrs = cooperative_launch() ? 1 : 0;
+    cfg.numAttrs = na;
     LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "scan kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return LS_OK;

@@ -204,11 +204,8 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     uint64_t *rnd = agg + M * S::W;
     const T *x = static_cast<const T *>(p.x);
     T *y = static_cast<T *>(p.y);
-    const uint32_t tag = call_tag(hdr);
     const int64_t my_tiles = (M - c + G - 1) / G;
     const int64_t full_tiles = p.n / TILE_ELEMS;
-    Header *xhdr = MULTI ? reinterpret_cast<Header *>(p.xchg) : nullptr;
-    const uint32_t xtag = MULTI ? call_tag(xhdr) : 0u;
 
     if (tid == 0) {
 #pragma unroll
@@ -221,6 +218,15 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
         fence_mbar_init();
     }
     __syncthreads();
+    // programmatic dependent launch: everything above overlaps the previous
+    // kernel's tail; no global memory is touched before this wait (it returns
+    // once that kernel has completed and flushed).  The next kernel may start
+    // launching right away: its blocks take SMs only as ours exit.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t tag = call_tag(hdr);
+    Header *xhdr = MULTI ? reinterpret_cast<Header *>(p.xchg) : nullptr;
+    const uint32_t xtag = MULTI ? call_tag(xhdr) : 0u;
 
     if (warp == W_PROD) {
         // ------------------------------------------------------------ producer
