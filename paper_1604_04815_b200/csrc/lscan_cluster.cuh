@@ -50,6 +50,13 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
 __device__ __forceinline__ void st_cluster_u64(uint32_t addr, uint64_t v) {
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
+// split cluster barrier (every thread of every CTA): the first phase only
+// guarantees every CTA of the cluster has started before anyone stores into
+// its shared memory, so it is relaxed and its latency hides behind the loads
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 // every thread of every CTA of the cluster; release/acquire orders the DSMEM
 // stores issued before the arrival with the loads after the wait
 __device__ __forceinline__ void cluster_sync_all() {
@@ -96,6 +103,7 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t r = cluster_ctarank();
     const uint32_t C = cluster_nctarank();
+    if (C > 1) cluster_arrive_relaxed();  // phase 1: "this CTA is running" (waited on before DSMEM stores)
     const int64_t b = blockIdx.x;        // tile index
     const int64_t k = b / C;             // cluster index
     const int64_t K = gridDim.x / C;     // clusters in the grid
@@ -149,6 +157,7 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
         run = j == 0 ? rt : OP::apply(run, rt);
     }
     if (lane == 0) warp_tot[warp] = run;
+    if (C > 1) cluster_wait();  // every CTA of the cluster has started: its shared memory may be written
     __syncthreads();
 
     // ---- warp totals -> exclusive warp prefixes; the block aggregate goes to

@@ -1,6 +1,11 @@
 """Small scans for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
-    python scripts/sanitize_case.py [all|full|partial|generic|reduce]
+    python scripts/sanitize_case.py [all|full|partial|generic|reduce|cluster]
+
+full / partial / generic run with the persistent kernel forced (small sizes
+would otherwise take the latency kernel); cluster runs the latency kernel on
+one cluster, several clusters (small, mid and large tiles), misaligned
+inputs and a carry.
 """
 import os
 import sys
@@ -12,6 +17,19 @@ from paper_1604_04815_b200 import scan as S  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
 for dt in (torch.int32, torch.float64):
+    if mode in ("all", "cluster"):
+        c = S.query_cluster(dt)
+        with S.force_path("cluster"):
+            for n in (5, c["block_elems"] * 3 + 7, c["one_cluster_elems"] + 11, c["mid_max_elems"] + 5):
+                for off in (0, 1):
+                    x = ((torch.arange(n + 1, dtype=dt, device="cuda") % 7) - 3)[off:off + n]
+                    for op in ("add", "max"):
+                        y = S.inclusive_scan(x, op=op)
+                        ref = torch.cumsum(x.double(), 0).to(dt) if op == "add" else torch.cummax(x, 0).values
+                        assert torch.equal(y, ref), (dt, n, "cluster", op)
+                        S.exclusive_scan(x, op=op, carry_in=x[:1].clone())
+    if mode == "cluster":
+        continue
     tile = S.query_config(dt, 1 << 20)["tile_elems"]
     sizes = {"full": (tile * 3, tile * 200), "partial": (5, tile * 3 + 7, 300_001),
              "generic": (tile * 3 + 7,), "reduce": (300_001,)}
@@ -27,10 +45,11 @@ for dt in (torch.int32, torch.float64):
             if m == "reduce":
                 S.reduce_sum(x)
                 continue
-            for op in ("add", "max"):
-                y = S.inclusive_scan(x, op=op)
-                ref = torch.cumsum(x.double(), 0).to(dt) if op == "add" else torch.cummax(x, 0).values
-                assert torch.equal(y, ref), (dt, n, m, op)
-                S.exclusive_scan(x, op=op)
+            with S.force_path("persistent"):
+                for op in ("add", "max"):
+                    y = S.inclusive_scan(x, op=op)
+                    ref = torch.cumsum(x.double(), 0).to(dt) if op == "add" else torch.cummax(x, 0).values
+                    assert torch.equal(y, ref), (dt, n, m, op)
+                    S.exclusive_scan(x, op=op)
 torch.cuda.synchronize()
 print("sanitize cases ok", mode)
