@@ -149,25 +149,31 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- ours --
 
-def time_device(fn, steps, warmup, stream, dist=None):
+def time_device(fn, steps, warmup, stream, dist=None, blocks=None):
     """W untimed steps, then exactly K steps between barrier+sync pairs,
-    timed with CUDA events on the launching stream; returns ms/step (max over ranks)."""
+    timed with CUDA events on the launching stream; returns ms/step (max over ranks).
+    ``blocks``: a list that receives the ms/step of up to 10 equal blocks of
+    the same K steps (events recorded inside the timed region, rank-local)."""
     import torch
     for _ in range(warmup):
         fn()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        fn()
-    e1.record(stream)
+    nb = 10 if blocks is not None and steps >= 10 else 1
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nb + 1)]
+    bounds = [steps * i // nb for i in range(nb + 1)]
+    evs[0].record(stream)
+    for b in range(nb):
+        for _ in range(bounds[b + 1] - bounds[b]):
+            fn()
+        evs[b + 1].record(stream)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ms = e0.elapsed_time(e1) / steps
+    ms = evs[0].elapsed_time(evs[-1]) / steps
+    if blocks is not None and nb > 1:
+        blocks.extend(evs[b].elapsed_time(evs[b + 1]) / (bounds[b + 1] - bounds[b]) for b in range(nb))
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -361,8 +367,9 @@ def run_ours(args):
     sampler = ClockSampler(local)
     for _ in range(args.warmup):
         step()
+    block_ms = []
     with sampler:
-        ms = time_device(step, args.steps, 0, stream, dist if use_dist else None)
+        ms = time_device(step, args.steps, 0, stream, dist if use_dist else None, blocks=block_ms)
     clocks = sampler.summary()
     # native launches per step, counted through the library's launch counter
     c0 = N.launch_count()
@@ -395,6 +402,11 @@ def run_ours(args):
                    "kernel_geometry": S.query_config(tdt, n)},
         "roofline": roofline,
         "gpu_launches": per_step * args.steps,
+        # best and median of 10 equal blocks of the same K timed steps (this rank)
+        "blocks_of_k": ({"blocks": len(block_ms),
+                         "best_gelems": round(total_elems / (min(block_ms) * 1e-3) * 1e-9, 2),
+                         "median_gelems": round(total_elems / (statistics.median(block_ms) * 1e-3) * 1e-9, 2)}
+                        if block_ms else None),
         "clocks": clocks,
         "validated": validated,
     }
