@@ -429,23 +429,35 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
     const DebugCfg dbg = debug_snapshot();
 
     const uintptr_t mx = (uintptr_t)x & 15u, my = (uintptr_t)y & 15u;
+    bool launched = false;
     if (use_cluster(*d, dt, n, dbg)) {
+        // a cluster grid the GPU cannot place right now (its GPCs held by
+        // other work) fails at launch without side effects: the persistent
+        // kernel takes the call instead
         st = launch_cluster(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl);
-    } else if (mx == 0 && my == 0) {
-        st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, true, dbg);
-    } else if (mx == my && n >= kSplitMinElems) {
-        // x and y share their misalignment (e.g. a slice scanned in place):
-        // the few head elements up to the 16-byte boundary go through the
-        // generic kernel, whose total carries into the TMA kernel for the rest
-        const int64_t head = (int64_t)((16u - mx) / (unsigned)es);
-        void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
-        st = launch_scan(*d, op, dt, x, y, head, carry_in, scratch, ws, s, excl, false, dbg);
-        if (st == LS_OK)
-            st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
-                             static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl, true,
-                             dbg);
-    } else {
-        st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, false, dbg);
+        launched = st == LS_OK;
+        if (!launched && dbg.force_path != 2) {
+            (void)cudaGetLastError();
+            st = LS_OK;
+        }
+    }
+    if (!launched && st == LS_OK) {
+        if (mx == 0 && my == 0) {
+            st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, true, dbg);
+        } else if (mx == my && n >= kSplitMinElems) {
+            // x and y share their misalignment (e.g. a slice scanned in place):
+            // the few head elements up to the 16-byte boundary go through the
+            // generic kernel, whose total carries into the TMA kernel for the rest
+            const int64_t head = (int64_t)((16u - mx) / (unsigned)es);
+            void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
+            st = launch_scan(*d, op, dt, x, y, head, carry_in, scratch, ws, s, excl, false, dbg);
+            if (st == LS_OK)
+                st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
+                                 static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl,
+                                 true, dbg);
+        } else {
+            st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, false, dbg);
+        }
     }
     if (st != LS_OK) return st;
     if (dbg.armed()) return read_device_error(ws, s, true);
