@@ -622,11 +622,16 @@ static ls_status scan_multi_impl(ls_op op, ls_dtype dt, const void *x, void *y, 
     cfg.blockDim = dim3((unsigned)L.threads);
     cfg.dynamicSmemBytes = L.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    // programmatic dependent launch as for the single-GPU kernel: the wait
+    // precedes every global access, and the exchange region's parity double
+    // buffer already separates consecutive calls across GPUs
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     LS_CUDA(cudaLaunchKernelEx(&cfg, L.fn, p), "multi scan kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     // no debug synchronisation here: the GPUs of one call must all be in
