@@ -76,3 +76,55 @@ def test_sharded_scan_gloo(tmp_path, world, tok, exclusive):
     else:
         # the carry is folded in rank order: identical to the one-shot fold
         assert oracle.validate_output(x, y, ref=ref, exclusive=exclusive) is None
+
+
+def _cyclic_worker(rank, world, port, n_local, stripe, tok, outdir):
+    """Host logic of the fused block-cyclic path without a GPU:
+    ``cyclic_layout`` maps this rank's share to global indices, the oracle
+    scans the global array, and ``check_cyclic`` (the bench's exact self-check
+    of the fused kernel) must accept the right answer and reject corruptions
+    of an interior element and of a stripe head."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+
+        from paper_1604_04815_b200.distributed import check_cyclic, cyclic_layout
+
+        class Scanner:  # the attributes check_cyclic reads
+            pass
+        sc = Scanner()
+        sc.world, sc.rank, sc.group, sc.stripe_elems = world, rank, None, stripe
+        total = n_local * world
+        xg = oracle.generate_input(total, tok, [5, total])
+        yg = oracle.sequential_scan(xg)
+        gidx = cyclic_layout(n_local, world, stripe)(rank, np.arange(n_local))
+        # every global index appears exactly once over the ranks
+        np.save(os.path.join(outdir, f"idx{rank}.npy"), gidx)
+        x = torch.from_numpy(xg[gidx].copy())
+        y = torch.from_numpy(yg[gidx].copy())
+        results = [check_cyclic(sc, x, y)]
+        bad = y.clone()
+        bad[n_local // 2 + 1] += 1  # interior element (on every rank)
+        results.append(check_cyclic(sc, x, bad))
+        bad = y.clone()
+        if rank == world - 1:
+            bad[stripe] += 1  # head of this rank's second stripe only
+        results.append(check_cyclic(sc, x, bad))
+        np.save(os.path.join(outdir, f"res{rank}.npy"), np.array(results))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,tok,n_local,stripe", [(2, "i32", 10_000, 1024), (3, "i64", 9_001, 1000),
+                                                      (4, "i32", 4_096, 512)])
+def test_cyclic_layout_and_check_gloo(tmp_path, world, tok, n_local, stripe):
+    port = _free_port()
+    mp.start_processes(_cyclic_worker, args=(world, port, n_local, stripe, tok, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    idx = np.concatenate([np.load(tmp_path / f"idx{r}.npy") for r in range(world)])
+    assert np.array_equal(np.sort(idx), np.arange(n_local * world))
+    for r in range(world):
+        ok, bad_interior, bad_head = np.load(tmp_path / f"res{r}.npy")
+        assert ok and not bad_interior and not bad_head, r
