@@ -455,6 +455,23 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
                 st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
                                  static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl,
                                  true, dbg);
+        } else if (n >= kSplitMinElems) {
+            // x and y misaligned differently: copy x into y (the copy engine
+            // handles any alignment at close to full bandwidth), then scan y
+            // in place — aligned, or congruently misaligned with itself.
+            // 4N bytes instead of the generic kernel's 2N at a quarter of the speed.
+            LS_CUDA(cudaMemcpyAsync(y, x, (size_t)n * es, cudaMemcpyDeviceToDevice, s), "realigning copy");
+            if (my == 0) {
+                st = launch_scan(*d, op, dt, y, y, n, carry_in, total_out, ws, s, excl, true, dbg);
+            } else {
+                const int64_t head = (int64_t)((16u - my) / (unsigned)es);
+                void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
+                st = launch_scan(*d, op, dt, y, y, head, carry_in, scratch, ws, s, excl, false, dbg);
+                if (st == LS_OK)
+                    st = launch_scan(*d, op, dt, static_cast<uint8_t *>(y) + head * es,
+                                     static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s,
+                                     excl, true, dbg);
+            }
         } else {
             st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, false, dbg);
         }

@@ -274,3 +274,29 @@ def test_largest_size_checksum(S1, oracle_lib):
     ref, _ = oracle_lib.c_sequential_scan(x)
     y = S1.inclusive_scan(torch.from_numpy(x).cuda()).cpu().numpy()
     assert sha16(y) == sha16(ref)
+
+
+@pytest.mark.parametrize("tok", TOKS)
+@pytest.mark.parametrize("xoff,yoff", [(1, 0), (0, 1), (1, 2), (3, 1)])
+def test_noncongruent_misalignment_realigned(S1, oracle_lib, tok, xoff, yoff):
+    # x and y misaligned differently (n >= 2^20): realigning copy x -> y, then
+    # an in-place scan of y (aligned, or congruent with itself: split path)
+    es = 4 if tok in ("i32", "f32") else 8
+    if (xoff * es) % 16 == (yoff * es) % 16:
+        pytest.skip("congruent")
+    n = 2_000_003
+    x = oracle_lib.generate_input(n + xoff, tok, [xoff, yoff])[xoff:].copy()
+    xd = torch.empty(n + 4, dtype=TDT[tok], device="cuda")[xoff:xoff + n]
+    xd.copy_(torch.from_numpy(x))
+    yd = torch.empty(n + 4, dtype=TDT[tok], device="cuda")[yoff:yoff + n]
+    tot = torch.empty(1, dtype=TDT[tok], device="cuda")
+    c = torch.from_numpy(x[:1].copy()).cuda()
+    S1.inclusive_scan(xd, out=yd, total_out=tot)
+    check(x, yd.cpu().numpy(), oracle_lib, what=f"{tok} inclusive x+{xoff} y+{yoff}")
+    assert torch.equal(xd.cpu(), torch.from_numpy(x))  # input untouched
+    S1.exclusive_scan(xd, out=yd, carry_in=c)
+    xx = np.concatenate([x[:1], x]).astype(x.dtype)
+    want = oracle_lib.c_sequential_scan(xx)[0][:-1]
+    if tok[0] == "i":
+        assert np.array_equal(yd.cpu().numpy(), want)
+        assert tot.item() == oracle_lib.c_sequential_scan(x)[1]
