@@ -138,6 +138,7 @@ struct DevState {
     int sms = 0;
     int occ[4][kNumOps][2][2] = {};  // resident CTAs per SM [dtype][op][excl][fast]
     int occ_multi[4][kNumOps][2] = {};
+    int occ_shift[4][2] = {};
     int reduce_occ[4][kNumOps] = {};
     int cluster_max = 0;          // largest schedulable cluster of the latency kernel (0: path off)
     int cluster_capacity[kClusterGeoms] = {};  // co-resident clusters of that size per geometry (min over instances)
@@ -179,6 +180,19 @@ ls_status device_state(DevState **out) {
                             "occupancy query");
                     if (occm < 1) return fail(LS_ERR_CUDA, "multi scan kernel cannot be resident");
                     d.occ_multi[dt][op][ex] = occm;
+                }
+                if (op == 0) {
+                    for (int ex = 0; ex < 2; ++ex) {
+                        const Launch &L = k.shift[ex];
+                        LS_CUDA(cudaFuncSetAttribute((const void *)L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)L.smem),
+                                "cudaFuncSetAttribute(max dynamic smem)");
+                        int occs = 0;
+                        LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, (const void *)L.fn, L.threads,
+                                                                              L.smem),
+                                "occupancy query");
+                        d.occ_shift[dt][ex] = occs;
+                    }
                 }
                 int occ = 0;
                 LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.reduce_fn[op], kReduceThreads, 0),
@@ -357,12 +371,14 @@ bool use_cluster(const DevState &d, ls_dtype dt, int64_t n, const DebugCfg &dbg)
 }
 
 // One kernel launch of the fast (TMA, 16-byte aligned) or generic path.
+// x_shift > 0: the add kernel over a misaligned x (x_shift bytes past a
+// 16-byte boundary; n a whole number of tiles)
 ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
                       const void *carry_in, void *total_out, void *ws, cudaStream_t s, bool excl, bool fast,
-                      const DebugCfg &dbg) {
-    const Launch &L = K(dt).scan[op][excl][fast];
+                      const DebugCfg &dbg, int x_shift = 0) {
+    const Launch &L = x_shift ? K(dt).shift[excl] : K(dt).scan[op][excl][fast];
     const int64_t M = num_tiles(dt, n, fast);
-    const int64_t cap = (int64_t)d.occ[dt][op][excl][fast] * d.sms;
+    const int64_t cap = (int64_t)(x_shift ? d.occ_shift[dt][excl] : d.occ[dt][op][excl][fast]) * d.sms;
     const int G = (int)std::min<int64_t>(M, cap);
     ScanParams p{};
     p.x = x;
@@ -379,6 +395,7 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     p.delay_scan_ns = dbg.delay_scan_ns;
     // a stalled tile without a watchdog would hang the chain forever
     p.stall_tile = dbg.spin_budget > 0 ? dbg.stall_tile : -1;
+    p.x_shift = x_shift;
 
     // Cooperative launch: the driver refuses a grid that cannot be fully
     // co-resident — the deadlock-freedom precondition of the persistent
@@ -455,6 +472,23 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
                 st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
                                  static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl,
                                  true, dbg);
+        } else if (my == 0 && op == LS_OP_ADD && n >= kSplitMinElems && d->occ_shift[dt][excl] > 0) {
+            // x misaligned, y aligned (a slice scanned into a fresh output):
+            // whole tiles by the shifted-window TMA kernel, the ragged end
+            // (< one tile) by the latency kernel with the head's total as carry
+            const int64_t te = tile_elems(dt, true);
+            const int64_t n_full = n / te * te;
+            const bool tail = n_full < n;
+            void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
+            st = launch_scan(*d, op, dt, x, y, n_full, carry_in, tail ? scratch : total_out, ws, s, excl, true, dbg,
+                             (int)mx);
+            if (st == LS_OK && tail) {
+                const void *xt = static_cast<const uint8_t *>(x) + n_full * es;
+                void *yt = static_cast<uint8_t *>(y) + n_full * es;
+                st = d->cluster_max ? launch_cluster(*d, op, dt, xt, yt, n - n_full, scratch, total_out, ws, s, excl)
+                                    : launch_scan(*d, op, dt, xt, yt, n - n_full, scratch, total_out, ws, s, excl,
+                                                  false, dbg);
+            }
         } else if (n >= kSplitMinElems) {
             // x and y misaligned differently: copy x into y (the copy engine
             // handles any alignment at close to full bandwidth), then scan y

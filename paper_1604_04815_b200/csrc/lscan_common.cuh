@@ -150,6 +150,8 @@ struct ScanParams {
     uint8_t *xchg;                 // this GPU's exchange region (header + 2 parities of slots)
     uint64_t *const *xchg_peers;   // device array: every GPU's exchange slot base (index = rank)
     int64_t xchg_rounds;           // round capacity per parity
+    // ---- x not 16-byte aligned (scan_ws2_kernel<..., SHIFT=true>) ----
+    int x_shift;                   // bytes x lies past the 16-byte boundary below it
 };
 
 // cross-GPU exchange region: [Header][parity 0: rounds x world slots][parity 1: ...]

@@ -15,6 +15,14 @@ Launch fast_launch() {
             scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(), C::kTileBytes, C::kStages};
 }
 
+template <typename T, bool EXCL>
+Launch shift_launch() {
+    using C = FastCfg<sizeof(T)>;
+    return {&scan_ws2_kernel<T, OpAdd, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true>,
+            (C::kScanWarps + 3) * 32, scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true>(),
+            C::kTileBytes, C::kStages};
+}
+
 template <typename T, typename OP, bool EXCL>
 Launch multi_launch() {
     using C = FastCfg<sizeof(T)>;
@@ -83,6 +91,8 @@ DtypeKernels make_kernels() {
     fill_op<T, OpAdd>(k);
     fill_op<T, OpMax>(k);
     fill_op<T, OpMin>(k);
+    k.shift[0] = shift_launch<T, false>();
+    k.shift[1] = shift_launch<T, true>();
     k.launch_reduce = &launch_reduce_t<T>;
     k.launch_carry = &launch_carry_t<T>;
     k.launch_stress = &launch_stress_t<T>;

@@ -80,6 +80,54 @@ __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
     return warp_reduce_fixed<T, OP>(OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3])));
 }
 
+// the same over a shifted window (SHIFT): the stage holds TILE_BYTES + 16
+// bytes from the 16-byte boundary below the tile, whose first `sh` elements
+// belong to the previous tile and whose last vector's first `sh` elements to
+// this one
+template <typename T, typename OP, int TILE_BYTES>
+__device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, int sh) {
+    constexpr int NV = TILE_BYTES / 16 / 32;
+    constexpr int PER = 16 / (int)sizeof(T);
+    static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
+    const T ident = OP::template identity<T>();
+    T acc[4] = {ident, ident, ident, ident};
+    const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
+#pragma unroll 2
+    for (int j = 0; j < NV; j += 4) {
+        Regs<T, 4> r;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r.q[u] = lds128(base + (uint32_t)(j + u) * 512u);
+        if (j == 0 && lane == 0) {
+#pragma unroll
+            for (int e = 0; e < PER; ++e)
+                if (e < sh) r.e[e] = ident;  // the previous tile's elements
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int e = 0; e < PER; ++e) acc[u] = OP::apply(acc[u], r.e[u * PER + e]);
+    }
+    T a = OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3]));
+    if (lane == 0) {
+        Regs<T, 1> r;
+        r.q[0] = lds128(smem_u32(st) + (uint32_t)TILE_BYTES);
+#pragma unroll
+        for (int e = 0; e < PER; ++e)
+            if (e < sh) a = OP::apply(a, r.e[e]);
+    }
+    return warp_reduce_fixed<T, OP>(a);
+}
+
+// 16 bytes starting `sw` 32-bit words into a (continuing into b), sw in 1..3
+__device__ __forceinline__ uint4 funnel_words(uint4 a, uint4 b, int sw) {
+    uint4 r;
+    r.x = sw == 1 ? a.y : (sw == 2 ? a.z : a.w);
+    r.y = sw == 1 ? a.z : (sw == 2 ? a.w : b.x);
+    r.z = sw == 1 ? a.w : (sw == 2 ? b.x : b.y);
+    r.w = sw == 1 ? b.x : (sw == 2 ? b.y : b.z);
+    return r;
+}
+
 template <typename T>
 struct LookbackOut {
     T r;    // R[k-1]
@@ -171,7 +219,8 @@ __device__ __forceinline__ uint64_t *xchg_slots(uint8_t *region, uint32_t xtag, 
            (int64_t)(xtag & 1u) * rounds_cap * world * Slot<T>::W;
 }
 
-template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL, bool MULTI = false>
+template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL, bool MULTI = false,
+          bool SHIFT = false>
 __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_kernel(const ScanParams p) {
     constexpr int SCAN_THREADS = SCAN_WARPS * 32;
     constexpr int V = TILE_BYTES / SCAN_THREADS / 16;  // rows (16-byte vectors) per lane
@@ -181,13 +230,18 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     constexpr int W_PROD = SCAN_WARPS, W_RED = SCAN_WARPS + 1, W_AUX = SCAN_WARPS + 2;
     constexpr int W_PUSH = SCAN_WARPS + 3, W_GCHAIN = SCAN_WARPS + 4;  // MULTI only, CTA G-1 only
     static_assert(V >= 1 && TILE_BYTES % (SCAN_THREADS * 16) == 0, "whole rows per lane");
+    static_assert(!(SHIFT && MULTI), "the shifted window is a single-GPU variant");
+    // SHIFT: x is not 16-byte aligned; every tile is loaded as a window of
+    // TILE_BYTES + 16 bytes from the boundary below it (all tiles full: the
+    // host scans the ragged end separately)
+    constexpr int STAGE_BYTES = TILE_BYTES + (SHIFT ? 16 : 0);
     static_assert(SCAN_WARPS >= 2 && ws2_threads<SCAN_WARPS, MULTI>() <= 1024, "too many warps");
     using S = Slot<T>;
     const T ident = OP::template identity<T>();
 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stages = smem;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * TILE_BYTES);  // data landed
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);  // data landed
     uint64_t *empty = full + STAGES;          // scanners + reducer done reading (2 arrivals)
     uint64_t *pre_ready = empty + STAGES;     // prefix written
     uint64_t *pre_free = pre_ready + STAGES;  // prefix consumed
@@ -235,8 +289,14 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
             const int64_t t0 = t * TILE_ELEMS;
-            uint8_t *sb = stages + s * TILE_BYTES;
-            if (t < full_tiles) {
+            uint8_t *sb = stages + s * STAGE_BYTES;
+            if constexpr (SHIFT) {
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                    tma_load_1d(sb, reinterpret_cast<const uint8_t *>(x) - p.x_shift + t * (int64_t)TILE_BYTES,
+                                STAGE_BYTES, &full[s], pol);
+                }
+            } else if (t < full_tiles) {
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[s], TILE_BYTES);
                     tma_load_1d(sb, x + t0, TILE_BYTES, &full[s], pol);
@@ -283,7 +343,10 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int64_t t = c + k * G;
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
             if (p.delay_red_ns > 0 && t % 3 == 1) debug_sleep(p.delay_red_ns);
-            const T a = LS_LAB_SKIP_REDUCE ? ident : reduce_stage<T, OP, TILE_BYTES>(stages + s * TILE_BYTES, lane);
+            const T a = LS_LAB_SKIP_REDUCE ? ident
+                        : SHIFT ? reduce_stage_shifted<T, OP, TILE_BYTES>(stages + s * STAGE_BYTES, lane,
+                                                                          p.x_shift / (int)sizeof(T))
+                                : reduce_stage<T, OP, TILE_BYTES>(stages + s * STAGE_BYTES, lane);
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&empty[s]);
@@ -418,9 +481,20 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             mbar_wait(&full[s], parity);
             if (p.delay_scan_ns > 0 && t % 3 == 2 && warp == (int)(t % SCAN_WARPS)) debug_sleep(p.delay_scan_ns);
             Regs<T, V> r;
-            const uint32_t sbase = smem_u32(stages + s * TILE_BYTES) + wbase;
+            const uint32_t sbase = smem_u32(stages + s * STAGE_BYTES) + wbase;
+            if constexpr (SHIFT) {
+                // logical vector v = window bytes [16v + shift, +16): two aligned
+                // reads and a word funnel (x is element-aligned, so the shift is
+                // a whole number of 32-bit words)
+                const int sw = p.x_shift >> 2;
 #pragma unroll
-            for (int j = 0; j < V; ++j) r.q[j] = lds128(sbase + (uint32_t)j * 512u);
+                for (int j = 0; j < V; ++j)
+                    r.q[j] = funnel_words(lds128(sbase + (uint32_t)j * 512u), lds128(sbase + (uint32_t)j * 512u + 16u),
+                                          sw);
+            } else {
+#pragma unroll
+                for (int j = 0; j < V; ++j) r.q[j] = lds128(sbase + (uint32_t)j * 512u);
+            }
             // per row j: lane-serial fold of the vector, inclusive warp scan
             T rex[V];   // exclusive prefix of this lane within row j (lane > 0)
             T rtot[V];  // row totals
@@ -527,10 +601,10 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     }
 }
 
-template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES>
+template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool SHIFT = false>
 constexpr size_t scan_ws2_smem_bytes() {
-    return (size_t)STAGES * TILE_BYTES + 4 * STAGES * 8 + STAGES * sizeof(T) + (STAGES + 1) * 4 +
-           2 * SCAN_WARPS * sizeof(T) + 32;
+    return (size_t)STAGES * (TILE_BYTES + (SHIFT ? 16 : 0)) + 4 * STAGES * 8 + STAGES * sizeof(T) +
+           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32;
 }
 
 }  // namespace lscan

@@ -300,3 +300,28 @@ def test_noncongruent_misalignment_realigned(S1, oracle_lib, tok, xoff, yoff):
     if tok[0] == "i":
         assert np.array_equal(yd.cpu().numpy(), want)
         assert tot.item() == oracle_lib.c_sequential_scan(x)[1]
+
+
+@pytest.mark.parametrize("tok", TOKS)
+@pytest.mark.parametrize("xoff", [1, 2, 3])
+def test_shifted_window_kernel(S1, oracle_lib, tok, xoff):
+    # x misaligned, y aligned, add: whole tiles by the shifted-window TMA kernel
+    # (two aligned smem reads and a word funnel per vector), the ragged end by
+    # the latency kernel with the head's total as carry
+    es = 4 if tok in ("i32", "f32") else 8
+    if (xoff * es) % 16 == 0:
+        pytest.skip("aligned")
+    T = S1.query_config(TDT[tok], 1 << 30)["tile_elems"]
+    for n in (200 * T, 200 * T + 1, 201 * T - 1, 1_000_003 + 300 * T):
+        x = oracle_lib.generate_input(n, tok, [xoff, n])
+        xd = torch.empty(n + 4, dtype=TDT[tok], device="cuda")[xoff:xoff + n]
+        xd.copy_(torch.from_numpy(x))
+        yd = torch.empty(n, dtype=TDT[tok], device="cuda")
+        assert xd.data_ptr() % 16 != 0 and yd.data_ptr() % 16 == 0
+        tot = torch.empty(1, dtype=TDT[tok], device="cuda")
+        S1.inclusive_scan(xd, out=yd, total_out=tot)
+        check(x, yd.cpu().numpy(), oracle_lib, what=f"{tok} shifted n={n}")
+        S1.exclusive_scan(xd, out=yd)
+        check(x, yd.cpu().numpy(), oracle_lib, exclusive=True, what=f"{tok} shifted excl n={n}")
+        if tok[0] == "i":
+            assert tot.item() == oracle_lib.c_sequential_scan(x)[1]
