@@ -1,4 +1,4 @@
-for mode in full partial generic reduce cluster; do
+for mode in full partial generic reduce cluster shifted; do
   timeout -s KILL 600 compute-sanitizer --tool racecheck --print-limit 5 python scripts/sanitize_case.py $mode > gpurun_out/racecheck_$mode.log 2>&1
   echo "racecheck $mode rc=$?"; tail -2 gpurun_out/racecheck_$mode.log
 done

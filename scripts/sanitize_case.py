@@ -1,6 +1,6 @@
 """Small scans for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
-    python scripts/sanitize_case.py [all|full|partial|generic|reduce|cluster]
+    python scripts/sanitize_case.py [all|full|partial|generic|reduce|cluster|shifted]
 
 full / partial / generic run with the persistent kernel forced (small sizes
 would otherwise take the latency kernel); cluster runs the latency kernel on
@@ -28,7 +28,15 @@ for dt in (torch.int32, torch.float64):
                         ref = torch.cumsum(x.double(), 0).to(dt) if op == "add" else torch.cummax(x, 0).values
                         assert torch.equal(y, ref), (dt, n, "cluster", op)
                         S.exclusive_scan(x, op=op, carry_in=x[:1].clone())
-    if mode == "cluster":
+    if mode in ("all", "shifted"):
+        # misaligned x, aligned y, n >= 2^20: the shifted-window TMA kernel + latency-kernel tail
+        tile = S.query_config(dt, 1 << 20)["tile_elems"]
+        for n in ((1 << 20) // tile * tile + 2 * tile, (1 << 20) + 7):
+            x = ((torch.arange(n + 1, dtype=dt, device="cuda") % 7) - 3)[1:]
+            y = S.inclusive_scan(x)
+            assert torch.equal(y, torch.cumsum(x.double(), 0).to(dt)), (dt, n, "shifted")
+            S.exclusive_scan(x)
+    if mode in ("cluster", "shifted"):
         continue
     tile = S.query_config(dt, 1 << 20)["tile_elems"]
     sizes = {"full": (tile * 3, tile * 200), "partial": (5, tile * 3 + 7, 300_001),
