@@ -4,6 +4,14 @@
 // The reference entry point this replaces is chained_scan(problem, config)
 // (chainscan/chained.py:316-357); see include/lscan.h for the per-function
 // mapping.  Kernels are instantiated per element type in lscan_inst_*.cu.
+//
+// Kernel selection per call (scan_impl):
+//   n <= cluster_limit (~10 MiB), debug hooks off  -> scan_cluster_kernel (any alignment)
+//   x, y 16-byte aligned                            -> scan_ws2_kernel (TMA, persistent)
+//   x, y misaligned alike, n >= 2^20                -> generic head + ws2 on the rest
+//   x misaligned, y aligned, add, n >= 2^20         -> ws2<SHIFT> on whole tiles + cluster tail
+//   otherwise misaligned, n >= 2^20                 -> realigning copy x -> y, then in place
+//   otherwise                                       -> scan_generic_kernel
 #include <cuda_runtime.h>
 
 #include <algorithm>
