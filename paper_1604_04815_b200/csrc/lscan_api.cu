@@ -24,6 +24,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <deque>
 #include <vector>
 
 #include "lscan.h"
@@ -152,7 +153,7 @@ struct DevState {
     int cluster_capacity[kClusterGeoms] = {};  // co-resident clusters of that size per geometry (min over instances)
 };
 std::mutex g_dev_mu;
-std::vector<DevState> g_dev;
+std::deque<DevState> g_dev;  // deque: growing it never moves the states other threads hold
 
 ls_status device_state(DevState **out) {
     int dev = 0;
