@@ -131,3 +131,31 @@ def test_on_block_hook_rejected():
     with pytest.raises(ValueError):
         P.chained_scan(P.ScanProblem(np.ones(10, dtype=np.int32), op),
                        P.ChainConfig(on_block=lambda w, b: None))
+
+
+def test_c8_throughput_over_sequential(oracle_lib):
+    # test_acceptance.py:265-290 (C8): the chained scan must beat the reference's
+    # sequential numpy fold by >= 1.5x at 2^26 — here through the numpy drop-in
+    # with pageable host arrays (PCIe and staging included) and on the device
+    import time
+    n = 1 << 26
+    x = oracle_lib.generate_input(n, "i32", [0, n])
+    op = P.make_operator("add", "i32")
+    y = P.chained_scan(P.ScanProblem(x, op))  # warm
+    t0 = time.perf_counter()
+    ref = oracle_lib.sequential_scan(x)
+    t_seq = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    y = P.chained_scan(P.ScanProblem(x, op))
+    t_ours = time.perf_counter() - t0
+    assert np.array_equal(y, ref)
+    assert t_seq / t_ours >= 1.5, (t_seq, t_ours)
+    xd = torch.from_numpy(x).cuda()
+    yd = P.inclusive_scan(xd)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        P.inclusive_scan(xd, out=yd)
+    torch.cuda.synchronize()
+    t_dev = (time.perf_counter() - t0) / 10
+    assert t_seq / t_dev >= 100, (t_seq, t_dev)
