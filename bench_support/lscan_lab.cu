@@ -25,7 +25,7 @@ int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t 
     default: f = &scan_ws2_kernel<int32_t, OpAdd, SW, TILE, STAGES, false>; break;
     }
     const size_t smem = scan_ws2_smem_bytes<int64_t, SW, TILE, STAGES>();
-    const int threads = (SW + 3) * 32;
+    const int threads = ws2_threads<SW, false>();
     if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int occ = 0, dev = 0, sms = 0;

@@ -11,7 +11,7 @@ namespace lscan {
 template <typename T, typename OP, bool EXCL>
 Launch fast_launch() {
     using C = FastCfg<sizeof(T)>;
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL>, (C::kScanWarps + 3) * 32,
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL>, ws2_threads<C::kScanWarps, false>(),
             scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(), C::kTileBytes, C::kStages};
 }
 
@@ -19,7 +19,7 @@ template <typename T, bool EXCL>
 Launch shift_launch() {
     using C = FastCfg<sizeof(T)>;
     return {&scan_ws2_kernel<T, OpAdd, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true>,
-            (C::kScanWarps + 3) * 32, scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true>(),
+            ws2_threads<C::kScanWarps, false>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true>(),
             C::kTileBytes, C::kStages};
 }
 

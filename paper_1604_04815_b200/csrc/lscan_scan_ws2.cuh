@@ -46,6 +46,11 @@
 #ifndef LS_LAB_SKIP_ROWSCAN
 #define LS_LAB_SKIP_ROWSCAN 0
 #endif
+// lab: per-phase clock64 totals (scanner warp 0, the producer and the look-back
+// warp), summed over CTAs into the workspace header's pad words
+#ifndef LS_LAB_TIMING
+#define LS_LAB_TIMING 0
+#endif
 #ifndef LS_LAB_SKIP_LOOKBACK
 #define LS_LAB_SKIP_LOOKBACK 0
 #endif
@@ -133,6 +138,7 @@ struct LookbackOut {
     T r;    // R[k-1]
     T sum;  // A[kG] (+) ... (+) A[kG+c-1]
     T own;  // A[t]
+    int polls = 0;  // re-polls after the first pass (lab statistics)
 };
 
 // One look-back step for tile t = k*G + c, every load in flight at once: the
@@ -150,6 +156,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
     const int64_t first = k * (int64_t)G;
     T acc = ident, own = ident, r = ident;
     int64_t probes = 0;
+    int polls = 0;
     bool r_pending = need_r;
     uint64_t rw[S::W];
     if (need_r) S::load(rnd, r_idx, rw);
@@ -186,6 +193,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
                 break;
             }
             __nanosleep(LS_LOOKBACK_SLEEP_NS);
+            ++polls;
             if (r_pending) S::load(rnd, r_idx, rw);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -204,6 +212,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
     o.sum = warp_reduce_fixed<T, OP>(acc);
     o.r = r;
     o.own = want_own ? __shfl_sync(0xffffffffu, own, c & 31) : ident;
+    o.polls = polls;
     return o;
 }
 
@@ -252,6 +261,8 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
+    long long lab_t[6] = {0, 0, 0, 0, 0, 0};  // LS_LAB_TIMING only
+    long long lab_polls = 0, lab_chain = 0;
     const int64_t M = p.num_tiles;
     Header *hdr = reinterpret_cast<Header *>(p.ws);
     uint64_t *agg = reinterpret_cast<uint64_t *>(p.ws + kSlotBase);
@@ -333,7 +344,9 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
         };
         for (int64_t k = 0; k < STAGES && k < my_tiles; ++k) load_tile(k);
         for (int64_t k = 0; k + STAGES < my_tiles; ++k) {
+            long long tw = LS_LAB_TIMING ? clock64() : 0;
             mbar_wait(&empty[k % STAGES], (uint32_t)((k / STAGES) & 1));
+            if (LS_LAB_TIMING) lab_t[4] += clock64() - tw;  // producer waiting for a free stage
             load_tile(k + STAGES);
         }
     } else if (warp == W_RED) {
@@ -385,10 +398,16 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                 // R[k-1]: the caller's carry in round 0, the chain owner's register,
                 // or the published round slot for everyone else
                 const bool need_r = k > 0 && c != G - 1;
+                const long long tl = LS_LAB_TIMING ? clock64() : 0;
                 const LookbackOut<T> lb =
-                    LS_LAB_SKIP_LOOKBACK ? LookbackOut<T>{ident, ident, ident}
+                    LS_LAB_SKIP_LOOKBACK ? LookbackOut<T>{ident, ident, ident, 0}
                                          : aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, k - 1, chain, tag, lane,
                                                                p.spin_budget, hdr, (uint32_t)t);
+                if (LS_LAB_TIMING) {
+                    lab_t[5] += clock64() - tl;  // look-back of one tile
+                    lab_polls += lb.polls;
+                    if (c == G - 1) lab_chain += clock64() - tl;
+                }
                 T base;
                 if (k == 0) { has = have_carry; base = r_prev; }
                 else if (c == G - 1) { has = true; base = r_prev; }
@@ -478,7 +497,9 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int s = (int)(k % STAGES);
             const uint32_t parity = (uint32_t)((k / STAGES) & 1);
             const int64_t t = c + k * G;
+            long long tm0 = LS_LAB_TIMING ? clock64() : 0;
             mbar_wait(&full[s], parity);
+            long long tm1 = LS_LAB_TIMING ? clock64() : 0;
             if (p.delay_scan_ns > 0 && t % 3 == 2 && warp == (int)(t % SCAN_WARPS)) debug_sleep(p.delay_scan_ns);
             Regs<T, V> r;
             const uint32_t sbase = smem_u32(stages + s * STAGE_BYTES) + wbase;
@@ -529,6 +550,7 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             }
             if (lane == 0) warp_tot[warp] = run;
             named_bar_sync(1, SCAN_THREADS);  // (A) stage fully read; warp totals visible
+            long long tm2 = LS_LAB_TIMING ? clock64() : 0;
             if (tid == 0) {
                 mbar_arrive(&empty[s]);
                 if (k > 0) mbar_arrive(&pre_free[(k - 1) % STAGES]);
@@ -546,6 +568,7 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             }
             mbar_wait(&pre_ready[s], parity);
             named_bar_sync(1, SCAN_THREADS);  // (B)
+            long long tm3 = LS_LAB_TIMING ? clock64() : 0;
             // carry into the first element of each of this lane's rows:
             //   tile prefix (+) warps before (+) rows before (+) lanes before
             bool has0 = pre_has[s] != 0;
@@ -581,9 +604,27 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                         if (vec * PER + e < valid) yt[vec * PER + e] = r.e[j * PER + e];
                 }
             }
+            if (LS_LAB_TIMING && tid == 0) {
+                const long long tm4 = clock64();
+                lab_t[0] += tm1 - tm0;  // waiting for the tile's data
+                lab_t[1] += tm2 - tm1;  // loads + row scans + barrier (A)
+                lab_t[2] += tm3 - tm2;  // warp-total scan, waiting for the prefix, barrier (B)
+                lab_t[3] += tm4 - tm3;  // fold + stores issued
+            }
         }
     }
 
+    if (LS_LAB_TIMING) {
+        unsigned long long *acc = reinterpret_cast<unsigned long long *>(hdr->pad);
+        if (tid == 0)
+            for (int i = 0; i < 4; ++i) atomicAdd(&acc[i], (unsigned long long)lab_t[i]);
+        if (warp == W_PROD && lane == 0) atomicAdd(&acc[4], (unsigned long long)lab_t[4]);
+        if (warp == W_AUX && lane == 0) {
+            atomicAdd(&acc[5], (unsigned long long)lab_t[5]);
+            atomicAdd(&acc[6], (unsigned long long)lab_polls);
+            atomicAdd(&acc[7], (unsigned long long)lab_chain);
+        }
+    }
     __syncthreads();
     if (tid == 0) {
         if constexpr (MULTI) {

@@ -79,6 +79,8 @@ def main():
     ap.add_argument("--labso", default="liblscanlab.so", help="lab library in bench_support/_build")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (device time, no host)")
     ap.add_argument("--product", action="store_true", help="also time the product call (scan.inclusive_scan)")
+    ap.add_argument("--timing", action="store_true",
+                    help="lab build with -DLS_LAB_TIMING=1: per-phase cycles per tile from the header pad")
     ap.add_argument("--sustain", type=int, default=0,
                     help="report this many consecutive blocks of --reps calls per config (drift under load)")
     args = ap.parse_args()
@@ -116,6 +118,20 @@ def main():
             res[f"cfg{cfg}_{CFG_NAMES[cfg]}_sustained_gelems"] = [round(n / (b * 1e-3) * 1e-9, 1) for b in blocks]
             res[f"cfg{cfg}_sm_mhz_after"] = effective_sm_mhz()
             continue
+        if args.timing:
+            step()
+            torch.cuda.synchronize()
+            ws[128 - 112:128].zero_()  # header pad words (bytes 16..127)
+            for _ in range(args.reps):
+                step()
+            torch.cuda.synchronize()
+            acc = ws[16:80].view(torch.int64).cpu().tolist()
+            tiles = -(-n // (8192 if es == 4 else 6144)) * args.reps
+            names = ["scan_wait_data", "scan_load_rowscan_barA", "scan_totals_prefix_barB", "scan_fold_store",
+                     "producer_wait_free_stage", "lookback_per_tile", "lookback_repolls_per_tile"]
+            res[f"cfg{cfg}_cycles_per_tile"] = {k: round(v / tiles, 2) for k, v in zip(names, acc)}
+            rounds = tiles / 148
+            res[f"cfg{cfg}_cycles_per_tile"]["chain_cta_lookback_per_round"] = round(acc[7] / rounds, 1)
         ms = graph_ms(step, args.reps) if args.graph else timeit(step, args.reps)
         res[f"cfg{cfg}_{CFG_NAMES[cfg]}"] = {
             "gelems": round(n / (ms * 1e-3) * 1e-9, 1), "gbs": round(2 * n * es / (ms * 1e-3) / 1e9, 1),
