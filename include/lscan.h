@@ -187,6 +187,11 @@ int ls_abi_version(void);
  * per tile, out[3] = pipeline stages, out[4] = resident CTAs per SM,
  * out[5] = SM count. */
 ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]);
+/* The multi-GPU kernel (ls_*_scan_multi) for n_local elements per GPU:
+ * out[0] = its default grid (CTAs per GPU), out[1] = elements per tile.  The
+ * block-cyclic stripe is grid * tile elements (GPU g's stripe k is global
+ * stripe k * world + g). */
+ls_status ls_query_multi_config(ls_dtype dt, int64_t n_local, int64_t out[2]);
 /* The latency kernel (small and mid n) on the current device: out[0] =
  * blocks per cluster (0 = unavailable), out[1] = elements per block (one
  * tile each) while n fits one cluster, out[2] = co-resident clusters of the

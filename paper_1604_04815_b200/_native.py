@@ -49,7 +49,7 @@ EXPORTED = [
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
     "ls_query_config", "ls_launch_count", "ls_xchg_bytes", "ls_inclusive_scan_multi", "ls_exclusive_scan_multi",
     "ls_device_alloc", "ls_device_free", "ls_ipc_get_handle", "ls_ipc_open", "ls_ipc_close", "ls_debug_slot_stress",
-    "ls_debug_force_path", "ls_query_cluster",
+    "ls_debug_force_path", "ls_query_cluster", "ls_query_multi_config",
 ]
 
 
@@ -143,6 +143,7 @@ def lib():
             "ls_debug_slot_stress": (ci, [ci, i64, ci, ctypes.POINTER(ctypes.c_int64)]),
             "ls_debug_force_path": (ci, [ci]),
             "ls_query_cluster": (ci, [ci, ctypes.POINTER(ctypes.c_int64)]),  # out[6]
+            "ls_query_multi_config": (ci, [ci, i64, ctypes.POINTER(ctypes.c_int64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -622,9 +622,15 @@ ls_status ls_carry_from_totals(ls_op op, ls_dtype dt, const void *totals, int64_
     return LS_OK;
 }
 
+// tiles of the multi-GPU kernel (its own geometry, MultiCfg)
+int64_t multi_tiles(ls_dtype dt, int64_t n) {
+    const int64_t te = K(dt).multi[0][0].tile_bytes / elem_size(dt);
+    return (n + te - 1) / te;
+}
+
 size_t ls_xchg_bytes(ls_dtype dt, int world, int64_t n_local) {
     if (!valid_dtype(dt) || world < 1 || n_local < 0) return 0;
-    const int64_t rounds = std::max<int64_t>(num_tiles(dt, n_local, true), 1);  // rounds <= tiles
+    const int64_t rounds = std::max<int64_t>(multi_tiles(dt, n_local), 1);  // rounds <= tiles
     const size_t sw = elem_size(dt) == 4 ? 8 : 16;
     const size_t bytes = kXchgSlotBase + 2 * (size_t)rounds * (size_t)world * sw;
     return (bytes + 255) & ~(size_t)255;
@@ -649,7 +655,7 @@ static ls_status scan_multi_impl(ls_op op, ls_dtype dt, const void *x, void *y, 
     DevState *d = nullptr;
     if ((st = device_state(&d)) != LS_OK) return st;
     const Launch &L = K(dt).multi[op][excl];
-    const int64_t M = num_tiles(dt, n, true);
+    const int64_t M = multi_tiles(dt, n);
     const int64_t cap = (int64_t)d->occ_multi[dt][op][excl] * d->sms;
     int64_t G = std::min<int64_t>(M, cap);
     if (grid > 0) {
@@ -818,6 +824,16 @@ ls_status ls_query_config(ls_dtype dt, int64_t n, int64_t out[6]) {
     out[3] = L.stages;
     out[4] = occ;
     out[5] = d->sms;
+    return LS_OK;
+}
+
+ls_status ls_query_multi_config(ls_dtype dt, int64_t n_local, int64_t out[2]) {
+    if (!valid_dtype(dt) || !out || n_local < 0) return fail(LS_ERR_INVALID_ARG, "bad arguments");
+    DevState *d = nullptr;
+    ls_status st = device_state(&d);
+    if (st != LS_OK) return st;
+    out[0] = std::min<int64_t>(std::max<int64_t>(multi_tiles(dt, n_local), 1), (int64_t)d->occ_multi[dt][0][0] * d->sms);
+    out[1] = K(dt).multi[0][0].tile_bytes / elem_size(dt);
     return LS_OK;
 }
 

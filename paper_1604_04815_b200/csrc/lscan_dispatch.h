@@ -23,6 +23,15 @@ template <>
 struct FastCfg<8> {
     static constexpr int kScanWarps = 12, kTileBytes = 49152, kStages = 4;
 };
+// the multi-GPU variant carries two more warps (pusher, global chain); the
+// 64-bit single-GPU geometry would then spill (17 warps leave ~100
+// registers a thread), so 64-bit multi-GPU scans use the 32-bit geometry's
+// 8 scanner warps and 32 KiB tiles (ls_query_multi_config reports them: the
+// block-cyclic layout follows the tile)
+template <int ES>
+struct MultiCfg : FastCfg<ES> {};
+template <>
+struct MultiCfg<8> : FastCfg<4> {};
 constexpr int kGenThreads = 512;  // generic (unaligned) path
 constexpr int kGenTileBytes = 32768;
 constexpr int kReduceThreads = 512;

@@ -25,7 +25,7 @@ Launch shift_launch() {
 
 template <typename T, typename OP, bool EXCL>
 Launch multi_launch() {
-    using C = FastCfg<sizeof(T)>;
+    using C = MultiCfg<sizeof(T)>;
     return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true>,
             ws2_threads<C::kScanWarps, true>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(),
             C::kTileBytes, C::kStages};

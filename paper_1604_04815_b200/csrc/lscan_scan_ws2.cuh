@@ -539,15 +539,10 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                 }
                 rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
             }
-            // serial row carry (Alg. 2): prefix of the rows before j
-            T rowpre[V];
+            // serial row carry (Alg. 2): the warp's total over its rows
             T run = rtot[0];
-            rowpre[0] = ident;
 #pragma unroll
-            for (int j = 1; j < V; ++j) {
-                rowpre[j] = run;
-                run = OP::apply(run, rtot[j]);
-            }
+            for (int j = 1; j < V; ++j) run = OP::apply(run, rtot[j]);
             if (lane == 0) warp_tot[warp] = run;
             named_bar_sync(1, SCAN_THREADS);  // (A) stage fully read; warp totals visible
             long long tm2 = LS_LAB_TIMING ? clock64() : 0;
@@ -577,11 +572,18 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             T *yt = y + t * (int64_t)TILE_ELEMS;
             const bool partial = t >= full_tiles;
             const int64_t valid = p.n - t * (int64_t)TILE_ELEMS;
+            // rows before j, folded as the rows are stored (the same left fold as
+            // the warp total above; no per-row array kept across the wait)
+            T rowpre = rtot[0];
 #pragma unroll
             for (int j = 0; j < V; ++j) {
                 bool has = has0;
                 T acc = wcarry;
-                if (j > 0) { acc = has ? OP::apply(acc, rowpre[j]) : rowpre[j]; has = true; }
+                if (j > 0) {
+                    acc = has ? OP::apply(acc, rowpre) : rowpre;
+                    has = true;
+                    if (j + 1 < V) rowpre = OP::apply(rowpre, rtot[j]);
+                }
                 if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
 #pragma unroll
                 for (int e = 0; e < PER; ++e) {

@@ -130,7 +130,7 @@ class CyclicScan:
         self.n_local = int(n_local)
         self.device = torch.device("cuda", torch.cuda.current_device())
         L = N.lib()
-        cfg = S.query_config(dtype, self.n_local)
+        cfg = S.query_multi_config(dtype, self.n_local)
         self.grid = int(grid) if grid > 0 else int(cfg["grid"])
         self.stripe_elems = self.grid * int(cfg["tile_elems"])
         meta = [None] * self.world

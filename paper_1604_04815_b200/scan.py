@@ -234,6 +234,15 @@ def query_config(dtype: torch.dtype, n: int) -> dict:
     return dict(zip(keys, (int(v) for v in out)))
 
 
+def query_multi_config(dtype: torch.dtype, n_local: int) -> dict:
+    """The multi-GPU kernel's default grid and tile (the block-cyclic stripe
+    is grid x tile elements)."""
+    import ctypes
+    out = (ctypes.c_int64 * 2)()
+    raise_for_status(N.lib().ls_query_multi_config(dtype_code(dtype), n_local, out))
+    return {"grid": int(out[0]), "tile_elems": int(out[1])}
+
+
 def query_cluster(dtype: torch.dtype) -> dict:
     """The latency kernel: blocks per cluster (0 = off), elements per block
     of the small and mid geometries, co-resident mid clusters, the largest n

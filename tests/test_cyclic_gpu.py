@@ -108,7 +108,7 @@ def assemble(parts, stripe):
 def test_virtual_gpus_match_global_scan(env, oracle_lib, tok, W):
     N, S, _ = env
     tdt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[tok]
-    tile = S.query_config(tdt, 1 << 20)["tile_elems"]
+    tile = S.query_multi_config(tdt, 1 << 20)["tile_elems"]
     sms = S.query_config(tdt, 1 << 20)["sms"]
     grid = sms // W
     stripe = grid * tile
@@ -132,7 +132,7 @@ def test_virtual_gpus_match_global_scan(env, oracle_lib, tok, W):
 def test_virtual_gpus_ops_exclusive_carry(env, oracle_lib, op):
     N, S, _ = env
     W = 2
-    tile = S.query_config(torch.int64, 1 << 20)["tile_elems"]
+    tile = S.query_multi_config(torch.int64, 1 << 20)["tile_elems"]
     grid = S.query_config(torch.int64, 1 << 20)["sms"] // W
     stripe = grid * tile
     n = 3 * stripe + 77
@@ -154,7 +154,7 @@ def test_repeated_calls_alternate_parity(env, oracle_lib):
     # alternating operators: results stay exact
     N, S, _ = env
     W = 2
-    tile = S.query_config(torch.int32, 1 << 20)["tile_elems"]
+    tile = S.query_multi_config(torch.int32, 1 << 20)["tile_elems"]
     grid = S.query_config(torch.int32, 1 << 20)["sms"] // W
     n = 2 * grid * tile + 5
     parts = [oracle_lib.generate_input(n, "i32", [g, 1]) for g in range(W)]
@@ -189,7 +189,7 @@ def test_two_pow_33_over_eight_virtual_gpus(env):
         ys, tots = v(xs)
     finally:
         v.close()
-    stripe = v.grid * S.query_config(torch.int32, n)["tile_elems"]
+    stripe = v.grid * S.query_multi_config(torch.int32, n)["tile_elems"]
     rounds = (n + stripe - 1) // stripe
     sums = torch.empty(rounds, W, dtype=torch.int64, device="cuda")
     for r in range(W):
