@@ -166,11 +166,12 @@ def test_graph_capture_replay(S, oracle_lib):
 
 
 @pytest.mark.parametrize("graph", [False, True])
-def test_dependent_chain(S, oracle_lib, graph):
+@pytest.mark.parametrize("n", [30_001, 3_000_017])
+def test_dependent_chain(S, oracle_lib, graph, n):
     """Back-to-back scans where each reads the previous one's output (the
     programmatic-dependent-launch overlap must keep the data dependency),
-    with a torch kernel in between every few calls; eager and graph-replayed."""
-    n = 30_001
+    with a torch kernel in between every few calls; eager and graph-replayed;
+    on the latency kernel (30 001) and the persistent kernel (3 000 017)."""
     x0 = oracle_lib.generate_input(n, "i32", [8, 8])
     bufs = [torch.from_numpy(x0).cuda()] + [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(12)]
 
