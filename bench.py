@@ -378,14 +378,20 @@ def run_ours(args):
     per_step = N.launch_count() - c0
     total_elems = n * world
     value = total_elems / (ms * 1e-3) * 1e-9
-    # dominant kernel: the scan kernel; at N=1 it is the whole step
-    scan_ms = ms if not use_dist else time_device(lambda: S.inclusive_scan(xd, out=yd), 20, 3, stream, None)
+    # dominant kernel: the scan kernel. At N=1 it is the whole step, and with
+    # the fused multi-GPU path it is too (one kernel per GPU per step, the
+    # exchange inside it); the NCCL path's step is reduce + all-gather + scan,
+    # so its scan kernel is timed on its own
+    fused = bool(use_dist and multi_path and multi_path.startswith("fused"))
+    scan_ms = ms if (not use_dist or fused) else time_device(lambda: S.inclusive_scan(xd, out=yd), 20, 3, stream,
+                                                              None)
     alg_bytes = 2 * n * es
     achieved = alg_bytes / (scan_ms * 1e-3) / 1e9
+    kernel = ("lscan::scan_ws2_kernel<MULTI> (fused block-cyclic, exchange over peer memory; per GPU)" if fused else
+              "lscan::scan_ws2_kernel (warp-specialised, TMA ring, register results)")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(tok, n),
-                "peak_source": peak_src, "kernel": "lscan::scan_ws2_kernel (warp-specialised, TMA ring, register results)",
-                "algorithmic_bytes_per_launch": alg_bytes}
+                "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(tok, n) if not use_dist else None,
+                "peak_source": peak_src, "kernel": kernel, "algorithmic_bytes_per_launch": alg_bytes}
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "Gelem/s", "n_gpus": world,
@@ -399,7 +405,8 @@ def run_ours(args):
                    "parallelism": (f"cyclic{world}" if multi_path and multi_path.startswith("fused")
                                    else f"shard{world}") if use_dist else "single",
                    "multi_gpu_path": multi_path, "multi_gpu_note": multi_note,
-                   "kernel_geometry": S.query_config(tdt, n)},
+                   "kernel_geometry": (dict(S.query_multi_config(tdt, n), world=world) if fused
+                                       else S.query_config(tdt, n))},
         "roofline": roofline,
         "gpu_launches": per_step * args.steps,
         # best and median of 10 equal blocks of the same K timed steps (this rank)
