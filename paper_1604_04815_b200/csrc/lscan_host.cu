@@ -126,7 +126,11 @@ int esize(ls_dtype dt) { return (dt == LS_I32 || dt == LS_F32) ? 4 : 8; }
 // bound the pageable pipeline well below PCIe.
 void parallel_memcpy(void *dst, const void *src, size_t bytes) {
     static const unsigned hw = std::thread::hardware_concurrency();
-    const unsigned nt = std::max(1u, std::min(8u, hw ? hw : 1u));
+    static const unsigned cap = [] {
+        const char *e = getenv("LSCAN_HOST_COPY_THREADS");
+        return e ? (unsigned)std::max(1, atoi(e)) : 16u;  // 16 measured 5 % faster than 8 (scripts/gpu_pageable_threads.sh)
+    }();
+    const unsigned nt = std::max(1u, std::min(cap, hw ? hw : 1u));
     if (bytes < ((size_t)4 << 20) || nt == 1) {
         memcpy(dst, src, bytes);
         return;
