@@ -248,11 +248,18 @@ def cpu_reference(tok: str, n: int, budget_s: float = 10.0):
         oracle.sequential_scan(xs)
         seq_t.append(time.perf_counter() - t0)
     med = statistics.median(ts)
+    # the reference's default geometry (L = 8192, chained.py:179-181), for comparison
+    t8 = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle.c_chained_scan(x, out=y, block_len=8192, workers=cores)
+        t8.append(time.perf_counter() - t0)
     return {
         "value": n / med * 1e-9, "unit": "Gelem/s", "cores": cores, "kind": "port",
         "sample": f"{tok} N={n} (the bench workload), C restatement of chained_scan, B={cores} threads, "
                   f"L=65536, median of {len(ts)} runs over {sum(ts):.1f} s",
         "numpy_sequential_gelems": xs.size / min(seq_t) * 1e-9,
+        "c_chained_L8192_gelems": n / statistics.median(t8) * 1e-9,
         "cpu_model": _cpu_model(),
     }
 
