@@ -9,6 +9,7 @@
 //     4: copy 1024 x 4 rows               5: copy 256 x 4 rows
 //     6: 256 x 16 rows (2 blocks/SM)       7: 256 x 8 rows (2 blocks/SM, product mid)
 //     8: int64 256 x 4 (product small)     9: int64 256 x 8 (product mid)
+//    10: int64 512 x 4 (2 blocks/SM)       11: int64 512 x 2
 //   lab_block_elems(variant) -> elements per block (int32)
 #include <cuda_runtime.h>
 
@@ -56,7 +57,9 @@ Var var(int v) {
     case 7: return {&scan_cluster_kernel<int32_t, OpAdd, false, 8, 256, 2>, 256, 8};
     // 64-bit elements, small and mid geometry
     case 8: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 256, 4>, 256, 4, 8};
-    default: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 256, 2>, 256, 8, 8};
+    case 9: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 256, 2>, 256, 8, 8};
+    case 10: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 512, 2>, 512, 4, 8};
+    default: return {&scan_cluster_kernel<int64_t, OpAdd, false, 2, 512, 4>, 512, 2, 8};
     }
 }
 }  // namespace
@@ -76,7 +79,7 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     const int C = (int)(tiles < 16 ? tiles : 16);
     const long long K = (tiles + C - 1) / C;
     if (C < 1 || (K > 1 && ((v == 4 || v == 5) || !ws))) return -1;
-    static bool init[16] = {};
+    static bool init[16] = {};  // variants 0..11
     if (!init[v]) {
         cudaFuncSetAttribute((const void *)w.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         init[v] = true;

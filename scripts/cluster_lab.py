@@ -16,8 +16,9 @@ from overhead_lab import graph_per_call  # noqa: E402
 from paper_1604_04815_b200 import scan as S  # noqa: E402
 
 NAMES = {0: "scan_256x4", 1: "scan_512x4", 2: "scan_256x8", 3: "scan_256x2", 4: "copy_1024x4", 5: "copy_256x4",
-         6: "scan_256x16_minb2", 7: "scan_256x8_minb2", 8: "i64_256x4", 9: "i64_256x8_minb2"}
-WIDE = {8, 9}
+         6: "scan_256x16_minb2", 7: "scan_256x8_minb2", 8: "i64_256x4", 9: "i64_256x8_minb2",
+         10: "i64_512x4_minb2", 11: "i64_512x2"}
+WIDE = {8, 9, 10, 11}
 
 
 def main():
