@@ -93,3 +93,28 @@ def test_two_pow_33_single_gpu(S):
         assert torch.equal(ys[1:] - ys[:-1], xs[1:])
         assert torch.equal(ys[:1], prev + xs[:1])
         prev = ys[-1:].clone()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("path", ["persistent", "shifted"])
+def test_beyond_2p31_elements(S, path):
+    """n = 2^31 + 5 (8 GiB of i32): past every 32-bit element index, on the
+    persistent kernel and on its shifted-window form (x offset by one element);
+    checked with the wrapping difference identity and a carried split."""
+    n = (1 << 31) + 5
+    g = torch.Generator(device="cuda").manual_seed(3)
+    buf = torch.randint(-1000, 1000, (n + 1,), dtype=torch.int32, device="cuda", generator=g)
+    x = buf[1:] if path == "shifted" else buf[:n]
+    y = S.inclusive_scan(x)
+    ok = bool(torch.equal(y[1:] - y[:-1], x[1:])) and int(y[0]) == int(x[0])
+    # the total equals the wrapped sum, through a two-piece carried scan too
+    cut = (1 << 31) - 7
+    t1 = torch.empty(1, dtype=torch.int32, device="cuda")
+    t2 = torch.empty(1, dtype=torch.int32, device="cuda")
+    S.inclusive_scan(x[:cut].clone(), total_out=t1)
+    del y
+    y2 = S.inclusive_scan(x[cut:].clone(), carry_in=t1, total_out=t2)
+    ok = ok and int(y2[-1]) == int(t2.item())
+    total = int(x.sum(dtype=torch.int64).item())
+    wrapped = (total + 2**31) % 2**32 - 2**31
+    assert ok and int(t2.item()) == wrapped
