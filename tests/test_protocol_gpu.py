@@ -127,3 +127,48 @@ def test_slot_handshake_stress(S, tok, code):
     reads, torn, regress = out
     assert reads >= 1_000_000
     assert torn == 0 and regress == 0
+
+
+def test_host_threads_and_streams_concurrently(S, oracle_lib):
+    """Four host threads, each on its own stream, scan different arrays of every
+    kernel's range (latency, multi-cluster, persistent) at the same time, and
+    the numpy drop-in runs beside them: per-(device, stream) workspaces and the
+    library's per-device state must keep them apart."""
+    import threading
+
+    import paper_1604_04815_b200 as P
+    sizes = [5_000, 400_000, 3_000_000, 12_000_000]
+    errors = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            tok = ("i32", "i64", "f32", "f64")[i]
+            x = oracle_lib.generate_input(sizes[i], tok, [i, 99])
+            with torch.cuda.stream(s):
+                xd = torch.from_numpy(x).to("cuda", non_blocking=False)
+                for _ in range(5):
+                    y = S.inclusive_scan(xd)
+                out = y.cpu().numpy()
+            msg = oracle_lib.validate_output(x, out)
+            if msg:
+                errors.append((tok, msg))
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    def dropin():
+        try:
+            x = oracle_lib.generate_input(3_000_001, "i32", [7, 7])
+            y = P.chained_scan(P.ScanProblem(x, P.make_operator("add", "i32")))
+            if not np.array_equal(y, oracle_lib.sequential_scan(x)):
+                errors.append(("dropin", "mismatch"))
+        except Exception as e:  # noqa: BLE001
+            errors.append(("dropin", repr(e)))
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)] + [threading.Thread(target=dropin)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
