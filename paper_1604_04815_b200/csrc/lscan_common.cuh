@@ -48,6 +48,7 @@ struct Elem<double> {
 // scan operators (ls_op in include/lscan.h: 0 add, 1 max, 2 min)
 struct OpAdd {
     static constexpr int code = 0;
+    static constexpr bool idempotent = false;
     template <typename T>
     __device__ __forceinline__ static T apply(T a, T b) {
         if constexpr (std::is_integral<T>::value) {
@@ -61,15 +62,42 @@ struct OpAdd {
     __device__ __forceinline__ static T identity() { return T(0); }
 };
 
+// (a >= b || isnan(a)) ? a : b  (GE) or the LE form, as one predicate chain:
+// FSETP.NAN, FSETP.GE.OR, FSEL — the C++ form compiles to a PLOP3 more
+template <typename T, bool GE>
+__device__ __forceinline__ T float_keep_a(T a, T b) {
+    T r;
+    if constexpr (std::is_same<T, float>::value) {
+        if constexpr (GE)
+            asm("{\n .reg .pred p;\n setp.nan.f32 p, %1, %1;\n setp.ge.or.f32 p, %1, %2, p;\n"
+                " selp.f32 %0, %1, %2, p;\n}" : "=f"(r) : "f"(a), "f"(b));
+        else
+            asm("{\n .reg .pred p;\n setp.nan.f32 p, %1, %1;\n setp.le.or.f32 p, %1, %2, p;\n"
+                " selp.f32 %0, %1, %2, p;\n}" : "=f"(r) : "f"(a), "f"(b));
+    } else {
+        if constexpr (GE)
+            asm("{\n .reg .pred p;\n setp.nan.f64 p, %1, %1;\n setp.ge.or.f64 p, %1, %2, p;\n"
+                " selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(a), "d"(b));
+        else
+            asm("{\n .reg .pred p;\n setp.nan.f64 p, %1, %1;\n setp.le.or.f64 p, %1, %2, p;\n"
+                " selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(a), "d"(b));
+    }
+    return r;
+}
+
 struct OpMax {
     static constexpr int code = 1;
+    static constexpr bool idempotent = true;  // x (+) x == x, bit for bit
     template <typename T>
     __device__ __forceinline__ static T apply(T a, T b) {
         if constexpr (std::is_integral<T>::value) {
             return a > b ? a : b;
         } else {
-            // numpy.maximum: a NaN operand propagates
-            return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+            // numpy.maximum: a NaN operand propagates (the first if both).
+            // a is kept when a >= b or a is NaN; a NaN b fails the compare and
+            // is selected.  FMNMX is not usable: it drops NaNs and orders -0 <
+            // +0, where numpy keeps the first of two equal operands
+            return float_keep_a<T, true>(a, b);
         }
     }
     template <typename T>
@@ -82,12 +110,13 @@ struct OpMax {
 
 struct OpMin {
     static constexpr int code = 2;
+    static constexpr bool idempotent = true;
     template <typename T>
     __device__ __forceinline__ static T apply(T a, T b) {
         if constexpr (std::is_integral<T>::value) {
             return a < b ? a : b;
         } else {
-            return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+            return float_keep_a<T, false>(a, b);  // numpy.minimum, as OpMax
         }
     }
     template <typename T>
@@ -292,7 +321,9 @@ __device__ __forceinline__ T warp_inclusive_scan(T v, int lane) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const T o = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v = OP::apply(o, v);
+        // lanes below d get their own value back; an idempotent operator
+        // absorbs it, so no lane predicate
+        if (OP::idempotent || lane >= d) v = OP::apply(o, v);
     }
     return v;
 }
