@@ -600,7 +600,9 @@ ls_status ls_reduce(ls_op op, ls_dtype dt, const void *x, int64_t n, void *total
     int64_t grid = std::min<int64_t>((n + per_cta - 1) / per_cta, (int64_t)d->reduce_occ[dt][op] * d->sms);
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, kMaxGrid));
     K(dt).launch_reduce(op, x, n, total_out, ws, (int)grid, s);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    // float max/min add the tie fix-up kernel (lscan_generic.cuh)
+    const bool ties = op != LS_OP_ADD && (dt == LS_F32 || dt == LS_F64);
+    g_launches.fetch_add(ties ? 2 : 1, std::memory_order_relaxed);
     LS_CUDA(cudaGetLastError(), "reduce kernel launch");
     return LS_OK;
 }

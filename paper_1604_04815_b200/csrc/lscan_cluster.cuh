@@ -209,9 +209,9 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
                             S::load(slots, j, w);
                         }
                     }
-                    acc = OP::apply(acc, v);
+                    acc = fold_chunk<T, OP>(acc, v);
                 }
-                const T g = warp_reduce_fixed<T, OP>(acc);
+                const T g = fold_finish<T, OP>(acc);
                 pre = has ? OP::apply(pre, g) : g;
                 has = true;
             }

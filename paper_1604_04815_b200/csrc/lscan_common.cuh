@@ -62,24 +62,28 @@ struct OpAdd {
     __device__ __forceinline__ static T identity() { return T(0); }
 };
 
-// (a >= b || isnan(a)) ? a : b  (GE) or the LE form, as one predicate chain:
-// FSETP.NAN, FSETP.GE.OR, FSEL — the C++ form compiles to a PLOP3 more
-template <typename T, bool GE>
+// numpy's float maximum / minimum (numpy 2.3, pinned by tests/test_ties_gpu.py):
+//   maximum(a, b) = (a > b || isnan(a)) ? a : b      minimum: a < b
+// equal operands give the RIGHT one (max(-0, +0) = +0, max(+0, -0) = -0) and a NaN
+// on the left wins over one on the right.  As one predicate chain: FSETP.NAN,
+// FSETP.GT.OR, FSEL (the C++ form compiles to a PLOP3 more).  FMNMX is not
+// usable: it drops NaNs and orders -0 < +0.
+template <typename T, bool GT>
 __device__ __forceinline__ T float_keep_a(T a, T b) {
     T r;
     if constexpr (std::is_same<T, float>::value) {
-        if constexpr (GE)
-            asm("{\n .reg .pred p;\n setp.nan.f32 p, %1, %1;\n setp.ge.or.f32 p, %1, %2, p;\n"
+        if constexpr (GT)
+            asm("{\n .reg .pred p;\n setp.nan.f32 p, %1, %1;\n setp.gt.or.f32 p, %1, %2, p;\n"
                 " selp.f32 %0, %1, %2, p;\n}" : "=f"(r) : "f"(a), "f"(b));
         else
-            asm("{\n .reg .pred p;\n setp.nan.f32 p, %1, %1;\n setp.le.or.f32 p, %1, %2, p;\n"
+            asm("{\n .reg .pred p;\n setp.nan.f32 p, %1, %1;\n setp.lt.or.f32 p, %1, %2, p;\n"
                 " selp.f32 %0, %1, %2, p;\n}" : "=f"(r) : "f"(a), "f"(b));
     } else {
-        if constexpr (GE)
-            asm("{\n .reg .pred p;\n setp.nan.f64 p, %1, %1;\n setp.ge.or.f64 p, %1, %2, p;\n"
+        if constexpr (GT)
+            asm("{\n .reg .pred p;\n setp.nan.f64 p, %1, %1;\n setp.gt.or.f64 p, %1, %2, p;\n"
                 " selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(a), "d"(b));
         else
-            asm("{\n .reg .pred p;\n setp.nan.f64 p, %1, %1;\n setp.le.or.f64 p, %1, %2, p;\n"
+            asm("{\n .reg .pred p;\n setp.nan.f64 p, %1, %1;\n setp.lt.or.f64 p, %1, %2, p;\n"
                 " selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(a), "d"(b));
     }
     return r;
@@ -93,10 +97,6 @@ struct OpMax {
         if constexpr (std::is_integral<T>::value) {
             return a > b ? a : b;
         } else {
-            // numpy.maximum: a NaN operand propagates (the first if both).
-            // a is kept when a >= b or a is NaN; a NaN b fails the compare and
-            // is selected.  FMNMX is not usable: it drops NaNs and orders -0 <
-            // +0, where numpy keeps the first of two equal operands
             return float_keep_a<T, true>(a, b);
         }
     }
@@ -328,13 +328,55 @@ __device__ __forceinline__ T warp_inclusive_scan(T v, int lane) {
     return v;
 }
 
+// Float max/min results depend on the ORDER of equal-comparing operands (-0 /
+// +0) and of NaNs: the sequential fold yields the rightmost of the maximal
+// elements, or the leftmost NaN.  Every combination of partial results for
+// these operators keeps sequence order; add and the integer operators (whose
+// equal operands are identical bits) keep their cheaper unordered forms.
+template <typename T, typename OP>
+__host__ __device__ constexpr bool order_sensitive() {
+    return OP::idempotent && std::is_floating_point<T>::value;
+}
+
+// the values whose bits an order-free reduction may get wrong
+template <typename T>
+__device__ __forceinline__ bool tie_class(T v) {
+    return v != v || v == (T)0;
+}
+
 // fixed xor-butterfly: every lane ends with bit-identical results because
-// each level combines a commutative pair
+// each level combines a commutative pair.  Order-sensitive operators: levels
+// from d = 1 up, the lower lane group always on the left, so every lane holds
+// v_0 (+) v_1 (+) ... (+) v_31 in lane order
 template <typename T, typename OP>
 __device__ __forceinline__ T warp_reduce_fixed(T v) {
+    if constexpr (order_sensitive<T, OP>()) {
+        const int lane = (int)(threadIdx.x & 31u);
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) v = OP::apply(v, __shfl_xor_sync(0xffffffffu, v, d));
+        for (int d = 1; d < 32; d <<= 1) {
+            const T o = __shfl_xor_sync(0xffffffffu, v, d);
+            v = (lane & d) ? OP::apply(o, v) : OP::apply(v, o);
+        }
+    } else {
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) v = OP::apply(v, __shfl_xor_sync(0xffffffffu, v, d));
+    }
     return v;
+}
+
+// acc (+) v_0 (+) ... (+) v_31 for lane-strided chunks (lane l holds element
+// 32 m + l of chunk m).  Order-free operators accumulate per lane and reduce
+// once at the end (finish); order-sensitive ones reduce each chunk in lane
+// order into a warp-uniform accumulator
+template <typename T, typename OP>
+__device__ __forceinline__ T fold_chunk(T acc, T v) {
+    if constexpr (order_sensitive<T, OP>()) return OP::apply(acc, warp_reduce_fixed<T, OP>(v));
+    else return OP::apply(acc, v);
+}
+template <typename T, typename OP>
+__device__ __forceinline__ T fold_finish(T acc) {
+    if constexpr (order_sensitive<T, OP>()) return acc;
+    else return warp_reduce_fixed<T, OP>(acc);
 }
 
 }  // namespace lscan

@@ -66,10 +66,13 @@ __device__ __forceinline__ bool round_lookback(const uint64_t *agg, const uint64
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = base + u * 32 + lane;
-            if (j < c) acc = OP::apply(acc, val[u]);  // lane-serial, ascending j
+            if constexpr (order_sensitive<T, OP>())
+                acc = fold_chunk<T, OP>(acc, j < c ? val[u] : OP::template identity<T>());  // slot order
+            else if (j < c)
+                acc = OP::apply(acc, val[u]);  // lane-serial, ascending j
         }
     }
-    const T asum = warp_reduce_fixed<T, OP>(acc);
+    const T asum = fold_finish<T, OP>(acc);
     bool has = false;
     T rp = OP::template identity<T>();
     if (r > 0) {
@@ -268,8 +271,46 @@ __global__ void __launch_bounds__(THREADS) reduce_kernel(const T *__restrict__ x
         v = warp_reduce_fixed<T, OP>(v);
         if (lane == 0) {
             *total_out = v;
+            if constexpr (order_sensitive<T, OP>())  // reduce_ties_kernel's search word
+                *reinterpret_cast<long long *>(&hdr->pad[2]) = v != v ? 0x7fffffffffffffffll : -1ll;
             st_relaxed_u32(&hdr->done, 0u);
         }
+    }
+}
+
+// Order-sensitive operators (float max/min): the reduction above combines out
+// of sequence order, exact except for the bits of a zero or NaN total.  For
+// those this kernel (launched right behind it) finds the element the
+// sequential fold returns — the rightmost zero, or the leftmost NaN — and
+// writes it as the total; otherwise every block returns at once.
+template <typename T, typename OP, int THREADS>
+__global__ void __launch_bounds__(THREADS) reduce_ties_kernel(const T *__restrict__ x, int64_t n, T *total_out,
+                                                              uint8_t *ws) {
+    __shared__ bool last;
+    Header *hdr = reinterpret_cast<Header *>(ws);
+    long long *best_word = reinterpret_cast<long long *>(&hdr->pad[2]);
+    const T a = *total_out;
+    if (!tie_class(a)) return;
+    const bool nan = a != a;
+    long long best = nan ? 0x7fffffffffffffffll : -1ll;
+    for (int64_t i = (int64_t)blockIdx.x * THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * THREADS) {
+        const T v = x[i];
+        if (nan ? v != v : v == (T)0) best = nan ? min(best, (long long)i) : max(best, (long long)i);
+    }
+    if (nan ? best != 0x7fffffffffffffffll : best >= 0) {
+        if (nan) atomicMin(best_word, best);
+        else atomicMax(best_word, best);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atom_add_acqrel_u32(&hdr->done, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        *total_out = x[*(volatile long long *)best_word];
+        st_relaxed_u32(&hdr->done, 0u);
     }
 }
 

@@ -68,6 +68,14 @@ void launch_reduce_t(int op, const void *x, int64_t n, void *total_out, void *ws
     if (op == OpMax::code) reduce_kernel<T, OpMax, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
     else if (op == OpMin::code) reduce_kernel<T, OpMin, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
     else reduce_kernel<T, OpAdd, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+    if constexpr (order_sensitive<T, OpMax>()) {
+        // float max/min: the tie fix-up behind it (every block returns at
+        // once unless the total is a zero or a NaN)
+        if (op == OpMax::code)
+            reduce_ties_kernel<T, OpMax, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+        else if (op == OpMin::code)
+            reduce_ties_kernel<T, OpMin, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+    }
 }
 
 template <typename T>

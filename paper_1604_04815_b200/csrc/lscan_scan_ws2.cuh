@@ -62,6 +62,32 @@ __device__ __forceinline__ void stg128(void *p, uint4 v) {
                  : "memory");
 }
 
+// Order-sensitive operators (float max/min, lscan_common.cuh): the reducers
+// below combine a tile out of sequence order, which is exact except for the
+// bits of a tie-class result (a zero or a NaN).  Then the tile is searched for
+// the element the sequential fold would return — the rightmost zero, or the
+// leftmost NaN — among the window's elements [lo, hi) (16-byte vectors, lane
+// strided).  Rare by construction: one extra pass only when the tile's
+// aggregate is a zero or a NaN.
+template <typename T, typename OP>
+__device__ __noinline__ T tile_ties(const uint8_t *st, int lane, T fast, int nvec, int lo, int hi) {
+    constexpr int PER = 16 / (int)sizeof(T);
+    const bool nan = fast != fast;
+    int best = nan ? 0x7fffffff : -1;
+    for (int v = lane; v < nvec; v += 32) {
+        Regs<T, 1> r;
+        r.q[0] = lds128(smem_u32(st) + (uint32_t)v * 16u);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int w = v * PER + e;
+            const T x = r.e[e];
+            if (w >= lo && w < hi && (nan ? x != x : x == (T)0)) best = nan ? min(best, w) : max(best, w);
+        }
+    }
+    best = nan ? __reduce_min_sync(0xffffffffu, best) : __reduce_max_sync(0xffffffffu, best);
+    return reinterpret_cast<const T *>(st)[best];
+}
+
 // reduce a whole shared-memory tile with one warp (lane-strided 16-byte
 // vectors, conflict-free), four independent accumulators, fixed order
 template <typename T, typename OP, int TILE_BYTES>
@@ -82,7 +108,10 @@ __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
 #pragma unroll
             for (int e = 0; e < PER; ++e) acc[u] = OP::apply(acc[u], r.e[u * PER + e]);
     }
-    return warp_reduce_fixed<T, OP>(OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3])));
+    const T a = warp_reduce_fixed<T, OP>(OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3])));
+    if constexpr (order_sensitive<T, OP>())
+        if (tie_class(a)) return tile_ties<T, OP>(st, lane, a, TILE_BYTES / 16, 0, TILE_BYTES / (int)sizeof(T));
+    return a;
 }
 
 // the same over a shifted window (SHIFT): the stage holds TILE_BYTES + 16
@@ -120,7 +149,11 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
         for (int e = 0; e < PER; ++e)
             if (e < sh) a = OP::apply(a, r.e[e]);
     }
-    return warp_reduce_fixed<T, OP>(a);
+    a = warp_reduce_fixed<T, OP>(a);
+    if constexpr (order_sensitive<T, OP>())
+        if (tie_class(a))
+            return tile_ties<T, OP>(st, lane, a, TILE_BYTES / 16 + 1, sh, sh + TILE_BYTES / (int)sizeof(T));
+    return a;
 }
 
 // 16 bytes starting `sw` 32-bit words into a (continuing into b), sw in 1..3
@@ -204,12 +237,17 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = base + u * 32 + lane;
-            if (j < c) acc = OP::apply(acc, val[u]);
-            else if (j == c && want_own) own = val[u];
+            if constexpr (order_sensitive<T, OP>()) {
+                acc = fold_chunk<T, OP>(acc, j < c ? val[u] : ident);  // slot order
+                if (j == c && want_own) own = val[u];
+            } else {
+                if (j < c) acc = OP::apply(acc, val[u]);
+                else if (j == c && want_own) own = val[u];
+            }
         }
     }
     LookbackOut<T> o;
-    o.sum = warp_reduce_fixed<T, OP>(acc);
+    o.sum = fold_finish<T, OP>(acc);
     o.r = r;
     o.own = want_own ? __shfl_sync(0xffffffffu, own, c & 31) : ident;
     o.polls = polls;

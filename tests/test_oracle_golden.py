@@ -186,3 +186,18 @@ def test_empty(oracle_lib):
         y, tot = oracle_lib.c_sequential_scan(x)
         assert y.size == 0 and tot == 0
         assert oracle_lib.c_chained_scan(x).size == 0
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_float_max_min_tie_semantics(oracle_lib, dt):
+    """Pins the numpy behaviour the GPU operators restate (lscan_common.cuh
+    float_keep_a): maximum(a, b) = (a > b || isnan(a)) ? a : b — equal operands
+    give the right one, a NaN on the left beats one on the right."""
+    z = np.array([-0.0, 0.0, -1.0, 0.0, -0.0], dt)
+    assert np.signbit(oracle_lib.sequential_scan(z, op="max")).tolist() == [True, False, False, False, True]
+    assert np.signbit(oracle_lib.sequential_scan(-z, op="min")).tolist() == [False, True, True, True, False]
+    qn = np.array([np.nan], dt)
+    x = np.array([1.0, -qn[0], qn[0], 3.0], dt)
+    for op in ("max", "min"):
+        y = oracle_lib.sequential_scan(x, op=op)
+        assert not np.isnan(y[0]) and np.isnan(y[1:]).all() and np.signbit(y[1:]).all(), op
