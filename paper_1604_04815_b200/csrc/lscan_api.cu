@@ -9,8 +9,8 @@
 //   n <= cluster_limit (~10 MiB), debug hooks off  -> scan_cluster_kernel (any alignment)
 //   x, y 16-byte aligned                            -> scan_ws2_kernel (TMA, persistent)
 //   x, y misaligned alike, n >= 2^20                -> generic head + ws2 on the rest
-//   x misaligned, y aligned, add, n >= 2^20         -> ws2<SHIFT> on whole tiles + cluster tail
-//   otherwise misaligned, n >= 2^20                 -> realigning copy x -> y, then in place
+//   x, y misaligned differently, n >= 2^20          -> ws2<SHIFT> (one launch: y's head folded
+//                                                      into the carry, shifted x windows)
 //   otherwise                                       -> scan_generic_kernel
 #include <cuda_runtime.h>
 
@@ -147,7 +147,7 @@ struct DevState {
     int sms = 0;
     int occ[4][kNumOps][2][2] = {};  // resident CTAs per SM [dtype][op][excl][fast]
     int occ_multi[4][kNumOps][2] = {};
-    int occ_shift[4][2] = {};
+    int occ_shift[4][kNumOps][2] = {};
     int reduce_occ[4][kNumOps] = {};
     int cluster_max = 0;          // largest schedulable cluster of the latency kernel (0: path off)
     int cluster_capacity[kClusterGeoms] = {};  // co-resident clusters of that size per geometry (min over instances)
@@ -190,18 +190,15 @@ ls_status device_state(DevState **out) {
                     if (occm < 1) return fail(LS_ERR_CUDA, "multi scan kernel cannot be resident");
                     d.occ_multi[dt][op][ex] = occm;
                 }
-                if (op == 0) {
-                    for (int ex = 0; ex < 2; ++ex) {
-                        const Launch &L = k.shift[ex];
-                        LS_CUDA(cudaFuncSetAttribute((const void *)L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)L.smem),
-                                "cudaFuncSetAttribute(max dynamic smem)");
-                        int occs = 0;
-                        LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, (const void *)L.fn, L.threads,
-                                                                              L.smem),
-                                "occupancy query");
-                        d.occ_shift[dt][ex] = occs;
-                    }
+                for (int ex = 0; ex < 2; ++ex) {
+                    const Launch &L = k.shift[op][ex];
+                    LS_CUDA(cudaFuncSetAttribute((const void *)L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)L.smem),
+                            "cudaFuncSetAttribute(max dynamic smem)");
+                    int occs = 0;
+                    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, (const void *)L.fn, L.threads, L.smem),
+                            "occupancy query");
+                    d.occ_shift[dt][op][ex] = occs;
                 }
                 int occ = 0;
                 LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.reduce_fn[op], kReduceThreads, 0),
@@ -380,14 +377,15 @@ bool use_cluster(const DevState &d, ls_dtype dt, int64_t n, const DebugCfg &dbg)
 }
 
 // One kernel launch of the fast (TMA, 16-byte aligned) or generic path.
-// x_shift > 0: the add kernel over a misaligned x (x_shift bytes past a
-// 16-byte boundary; n a whole number of tiles)
+// x_shift > 0: the shifted-window kernel over a misaligned x (x_shift bytes
+// past a 16-byte boundary; y aligned), after folding the head_n elements
+// just before x / y into the carry (and storing them)
 ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
                       const void *carry_in, void *total_out, void *ws, cudaStream_t s, bool excl, bool fast,
-                      const DebugCfg &dbg, int x_shift = 0) {
-    const Launch &L = x_shift ? K(dt).shift[excl] : K(dt).scan[op][excl][fast];
+                      const DebugCfg &dbg, int x_shift = 0, int head_n = 0) {
+    const Launch &L = x_shift ? K(dt).shift[op][excl] : K(dt).scan[op][excl][fast];
     const int64_t M = num_tiles(dt, n, fast);
-    const int64_t cap = (int64_t)(x_shift ? d.occ_shift[dt][excl] : d.occ[dt][op][excl][fast]) * d.sms;
+    const int64_t cap = (int64_t)(x_shift ? d.occ_shift[dt][op][excl] : d.occ[dt][op][excl][fast]) * d.sms;
     const int G = (int)std::min<int64_t>(M, cap);
     ScanParams p{};
     p.x = x;
@@ -405,6 +403,7 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     // a stalled tile without a watchdog would hang the chain forever
     p.stall_tile = dbg.spin_budget > 0 ? dbg.stall_tile : -1;
     p.x_shift = x_shift;
+    p.head_n = head_n;
 
     // Cooperative launch: the driver refuses a grid that cannot be fully
     // co-resident — the deadlock-freedom precondition of the persistent
@@ -481,40 +480,16 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
                 st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
                                  static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl,
                                  true, dbg);
-        } else if (my == 0 && op == LS_OP_ADD && n >= kSplitMinElems && d->occ_shift[dt][excl] > 0) {
-            // x misaligned, y aligned (a slice scanned into a fresh output):
-            // whole tiles by the shifted-window TMA kernel, the ragged end
-            // (< one tile) by the latency kernel with the head's total as carry
-            const int64_t te = tile_elems(dt, true);
-            const int64_t n_full = n / te * te;
-            const bool tail = n_full < n;
-            void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
-            st = launch_scan(*d, op, dt, x, y, n_full, carry_in, tail ? scratch : total_out, ws, s, excl, true, dbg,
-                             (int)mx);
-            if (st == LS_OK && tail) {
-                const void *xt = static_cast<const uint8_t *>(x) + n_full * es;
-                void *yt = static_cast<uint8_t *>(y) + n_full * es;
-                st = d->cluster_max ? launch_cluster(*d, op, dt, xt, yt, n - n_full, scratch, total_out, ws, s, excl)
-                                    : launch_scan(*d, op, dt, xt, yt, n - n_full, scratch, total_out, ws, s, excl,
-                                                  false, dbg);
-            }
-        } else if (n >= kSplitMinElems) {
-            // x and y misaligned differently: copy x into y (the copy engine
-            // handles any alignment at close to full bandwidth), then scan y
-            // in place — aligned, or congruently misaligned with itself.
-            // 4N bytes instead of the generic kernel's 2N at a quarter of the speed.
-            LS_CUDA(cudaMemcpyAsync(y, x, (size_t)n * es, cudaMemcpyDeviceToDevice, s), "realigning copy");
-            if (my == 0) {
-                st = launch_scan(*d, op, dt, y, y, n, carry_in, total_out, ws, s, excl, true, dbg);
-            } else {
-                const int64_t head = (int64_t)((16u - my) / (unsigned)es);
-                void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
-                st = launch_scan(*d, op, dt, y, y, head, carry_in, scratch, ws, s, excl, false, dbg);
-                if (st == LS_OK)
-                    st = launch_scan(*d, op, dt, static_cast<uint8_t *>(y) + head * es,
-                                     static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s,
-                                     excl, true, dbg);
-            }
+        } else if (n >= kSplitMinElems && d->occ_shift[dt][op][excl] > 0) {
+            // x and y misaligned differently (e.g. a slice scanned into a fresh
+            // output): one launch of the shifted-window TMA kernel, tiled on y's
+            // 16-byte boundaries (x read through windows from the boundary below
+            // each tile); the < 16 bytes of y before its first boundary are
+            // folded into the carry inside the kernel
+            const int64_t head = my ? (int64_t)((16u - my) / (unsigned)es) : 0;
+            const uint8_t *xb = static_cast<const uint8_t *>(x) + head * es;
+            st = launch_scan(*d, op, dt, xb, static_cast<uint8_t *>(y) + head * es, n - head, carry_in, total_out, ws,
+                             s, excl, true, dbg, (int)((uintptr_t)xb & 15u), (int)head);
         } else {
             st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, false, dbg);
         }

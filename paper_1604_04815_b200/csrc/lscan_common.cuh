@@ -181,6 +181,7 @@ struct ScanParams {
     int64_t xchg_rounds;           // round capacity per parity
     // ---- x not 16-byte aligned (scan_ws2_kernel<..., SHIFT=true>) ----
     int x_shift;                   // bytes x lies past the 16-byte boundary below it
+    int head_n;                    // SHIFT: elements before x / y scanned first (y's 16-byte head)
 };
 
 // cross-GPU exchange region: [Header][parity 0: rounds x world slots][parity 1: ...]

@@ -48,7 +48,7 @@ struct Launch {
 struct DtypeKernels {
     Launch scan[kNumOps][2][2];  // [op][exclusive][fast]
     Launch multi[kNumOps][2];    // [op][exclusive]: block-cyclic multi-GPU variant of the fast kernel
-    Launch shift[2];             // [exclusive]: add over a 16-byte-misaligned x (shifted TMA window)
+    Launch shift[kNumOps][2];    // [op][exclusive]: x 16 bytes misaligned, y aligned (shifted TMA window)
     Launch cluster[kNumOps][2][kClusterGeoms];  // [op][exclusive][small, mid, large]: latency kernel (any alignment)
     const void *reduce_fn[kNumOps];
     void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s);

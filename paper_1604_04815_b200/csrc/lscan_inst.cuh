@@ -15,10 +15,10 @@ Launch fast_launch() {
             scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(), C::kTileBytes, C::kStages};
 }
 
-template <typename T, bool EXCL>
+template <typename T, typename OP, bool EXCL>
 Launch shift_launch() {
     using C = FastCfg<sizeof(T)>;
-    return {&scan_ws2_kernel<T, OpAdd, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true>,
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true>,
             ws2_threads<C::kScanWarps, false>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true>(),
             C::kTileBytes, C::kStages};
 }
@@ -57,6 +57,8 @@ void fill_op(DtypeKernels &k) {
     k.scan[OP::code][1][0] = generic_launch<T, OP, true>();
     k.multi[OP::code][0] = multi_launch<T, OP, false>();
     k.multi[OP::code][1] = multi_launch<T, OP, true>();
+    k.shift[OP::code][0] = shift_launch<T, OP, false>();
+    k.shift[OP::code][1] = shift_launch<T, OP, true>();
     k.reduce_fn[OP::code] = (const void *)&reduce_kernel<T, OP, kReduceThreads>;
 }
 
@@ -99,8 +101,6 @@ DtypeKernels make_kernels() {
     fill_op<T, OpAdd>(k);
     fill_op<T, OpMax>(k);
     fill_op<T, OpMin>(k);
-    k.shift[0] = shift_launch<T, false>();
-    k.shift[1] = shift_launch<T, true>();
     k.launch_reduce = &launch_reduce_t<T>;
     k.launch_carry = &launch_carry_t<T>;
     k.launch_stress = &launch_stress_t<T>;

@@ -339,11 +339,44 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int64_t t = c + k * G;
             const int64_t t0 = t * TILE_ELEMS;
             uint8_t *sb = stages + s * STAGE_BYTES;
-            if constexpr (SHIFT) {
+            // SHIFT: a window is TILE_ELEMS + PER elements from the boundary
+            // below the tile; it is TMA'd whole only when x backs all of it
+            if (SHIFT && p.x_shift / (int)sizeof(T) + (p.n - t0) >= TILE_ELEMS + PER) {
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
                     tma_load_1d(sb, reinterpret_cast<const uint8_t *>(x) - p.x_shift + t * (int64_t)TILE_BYTES,
                                 STAGE_BYTES, &full[s], pol);
+                }
+            } else if (SHIFT) {
+                // a window running past x's end (the last tile or two): window
+                // elements [0, sh + n - t0) hold data (the first sh the previous
+                // tile's); their 16-byte-aligned prefix by TMA, the ragged vector
+                // by plain loads, the rest identity — never reading past x's end
+                const int sh = p.x_shift / (int)sizeof(T);
+                const int64_t wvalid = sh + (p.n - t0);
+                const uint32_t bulk = (uint32_t)((wvalid * (int64_t)sizeof(T)) & ~(int64_t)15);
+                const int vfirst = (int)(bulk / 16);
+                const uint32_t sbase = smem_u32(sb);
+                const uint4 iv = identity_vec<T, OP>();
+                for (int v = vfirst + 1 + lane; v < STAGE_BYTES / 16; v += 32) sts128(sbase + (uint32_t)v * 16u, iv);
+                if (lane == 0) {
+                    Regs<T, 1> rv;
+#pragma unroll
+                    for (int e = 0; e < PER; ++e) {
+                        const int64_t w = (int64_t)vfirst * PER + e;
+                        rv.e[e] = (w >= sh && w < wvalid) ? x[t0 + w - sh] : ident;
+                    }
+                    sts128(sbase + (uint32_t)vfirst * 16u, rv.q[0]);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    if (bulk) {
+                        mbar_arrive_expect_tx(&full[s], bulk);
+                        tma_load_1d(sb, reinterpret_cast<const uint8_t *>(x) - p.x_shift + t * (int64_t)TILE_BYTES, bulk,
+                                    &full[s], pol);
+                    } else {
+                        mbar_arrive(&full[s]);
+                    }
                 }
             } else if (t < full_tiles) {
                 if (lane == 0) {
@@ -413,8 +446,22 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     } else if (warp == W_AUX) {
         // ----------------------------------------------------------- look-back
         const T *carry_in = static_cast<const T *>(p.carry_in);
-        const bool have_carry = carry_in != nullptr;
+        bool have_carry = carry_in != nullptr;
         T r_prev = have_carry ? *carry_in : ident;  // R[k-1] as known to CTA G-1 (the chain owner)
+        if constexpr (SHIFT) {
+            // y's head (the < 16 bytes before the aligned y this kernel tiles):
+            // every CTA folds it into the carry, in sequence order; CTA 0
+            // stores it.  One launch for any alignment
+            const T *hx = x - p.head_n;
+            T *hy = y - p.head_n;
+            for (int i = 0; i < p.head_n; ++i) {
+                const T v = hx[i];
+                const T before = r_prev;
+                r_prev = have_carry ? OP::apply(r_prev, v) : v;
+                if (c == 0 && lane == 0) hy[i] = EXCL ? (have_carry ? before : ident) : r_prev;
+                have_carry = true;
+            }
+        }
         for (int64_t k = 0; k < my_tiles; ++k) {
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;

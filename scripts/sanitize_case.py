@@ -31,11 +31,16 @@ for dt in (torch.int32, torch.float64):
     if mode in ("all", "shifted"):
         # misaligned x, aligned y, n >= 2^20: the shifted-window TMA kernel + latency-kernel tail
         tile = S.query_config(dt, 1 << 20)["tile_elems"]
-        for n in ((1 << 20) // tile * tile + 2 * tile, (1 << 20) + 7):
+        for n in ((1 << 20) // tile * tile + 2 * tile, (1 << 20) + 7, (1 << 20) // tile * tile + tile + 1):
+            # x ends exactly at its allocation's end (no slack to over-read)
             x = ((torch.arange(n + 1, dtype=dt, device="cuda") % 7) - 3)[1:]
             y = S.inclusive_scan(x)
             assert torch.equal(y, torch.cumsum(x.double(), 0).to(dt)), (dt, n, "shifted")
             S.exclusive_scan(x)
+            # y misaligned the other way: head folded in the kernel
+            yb = torch.empty(n + 1, dtype=dt, device="cuda")
+            S.inclusive_scan(x, out=yb[1:], op="max")
+            assert torch.equal(yb[1:], torch.cummax(x, 0).values), (dt, n, "shifted max")
     if mode in ("cluster", "shifted"):
         continue
     tile = S.query_config(dt, 1 << 20)["tile_elems"]

@@ -278,9 +278,9 @@ def test_largest_size_checksum(S1, oracle_lib):
 
 @pytest.mark.parametrize("tok", TOKS)
 @pytest.mark.parametrize("xoff,yoff", [(1, 0), (0, 1), (1, 2), (3, 1)])
-def test_noncongruent_misalignment_realigned(S1, oracle_lib, tok, xoff, yoff):
-    # x and y misaligned differently (n >= 2^20): realigning copy x -> y, then
-    # an in-place scan of y (aligned, or congruent with itself: split path)
+def test_noncongruent_misalignment_shifted(S1, oracle_lib, tok, xoff, yoff):
+    # x and y misaligned differently (n >= 2^20): one shifted-window launch,
+    # y's head folded into the carry in the kernel
     es = 4 if tok in ("i32", "f32") else 8
     if (xoff * es) % 16 == (yoff * es) % 16:
         pytest.skip("congruent")

@@ -101,3 +101,23 @@ def test_ties_reduce(S, tok, op, kind, n):
     got = S.reduce(torch.from_numpy(x).cuda(), op=op).cpu().numpy().reshape(-1)
     want = seq(x, op)[-1:]
     assert got.view(UI[tok])[0] == want.view(UI[tok])[0], (got, want)
+
+
+@pytest.mark.parametrize("tok", ["f32", "f64"])
+@pytest.mark.parametrize("op", ["max", "min"])
+@pytest.mark.parametrize("kind", ["dense_zeros", "sparse_zeros", "nans"])
+@pytest.mark.parametrize("xoff,yoff", [(1, 0), (0, 1), (3, 2)])
+def test_ties_misaligned(S, tok, op, kind, xoff, yoff):
+    """The shifted-window path (x and y misaligned differently): generic head,
+    shifted tiles, latency-kernel tail, totals carried between them."""
+    n = (1 << 21) + 5
+    x = make(kind, tok, op, n, 5)
+    xb = torch.empty(n + 4, dtype=TDT[tok], device="cuda")
+    xd = xb[xoff:xoff + n]
+    xd.copy_(torch.from_numpy(x))
+    yd = torch.empty(n + 4, dtype=TDT[tok], device="cuda")[yoff:yoff + n]
+    tot = torch.empty(1, dtype=TDT[tok], device="cuda")
+    S.inclusive_scan(xd, out=yd, total_out=tot, op=op)
+    ref = seq(x, op)
+    assert np.array_equal(yd.cpu().numpy().view(UI[tok]), ref.view(UI[tok]))
+    assert tot.cpu().numpy().view(UI[tok])[0] == ref[-1:].view(UI[tok])[0]
