@@ -151,6 +151,7 @@ struct DevState {
     int reduce_occ[4][kNumOps] = {};
     int cluster_max = 0;          // largest schedulable cluster of the latency kernel (0: path off)
     int cluster_capacity[kClusterGeoms] = {};  // co-resident clusters of that size per geometry (min over instances)
+    int64_t l2_bytes = 0;
 };
 std::mutex g_dev_mu;
 std::deque<DevState> g_dev;  // deque: growing it never moves the states other threads hold
@@ -163,6 +164,9 @@ ls_status device_state(DevState **out) {
     DevState &d = g_dev[dev];
     if (!d.init) {
         LS_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        int l2 = 0;
+        LS_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev), "L2 size");
+        d.l2_bytes = l2;
         for (int dt = 0; dt < 4; ++dt) {
             const DtypeKernels &k = K((ls_dtype)dt);
             for (int op = 0; op < kNumOps; ++op) {
@@ -376,6 +380,19 @@ bool use_cluster(const DevState &d, ls_dtype dt, int64_t n, const DebugCfg &dbg)
     return n <= cluster_limit(d, dt);
 }
 
+// Evict-normal TMA loads when the call's traffic fits well inside L2 (x then
+// stays for a caller that reads it again); LSCAN_L2_POLICY=first|normal
+// overrides for labs
+bool l2_policy_normal(const DevState &d, int64_t bytes) {
+    static const int mode = [] {
+        const char *e = getenv("LSCAN_L2_POLICY");
+        if (!e) return 0;
+        return strcmp(e, "first") == 0 ? 1 : (strcmp(e, "normal") == 0 ? 2 : 0);
+    }();
+    if (mode) return mode == 2;
+    return bytes <= d.l2_bytes * 3 / 4;
+}
+
 // One kernel launch of the fast (TMA, 16-byte aligned) or generic path.
 // x_shift > 0: the shifted-window kernel over a misaligned x (x_shift bytes
 // past a 16-byte boundary; y aligned), after folding the head_n elements
@@ -404,6 +421,7 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     p.stall_tile = dbg.spin_budget > 0 ? dbg.stall_tile : -1;
     p.x_shift = x_shift;
     p.head_n = head_n;
+    p.l2_resident = l2_policy_normal(d, 2 * n * (int64_t)elem_size(dt)) ? 1 : 0;
 
     // Cooperative launch: the driver refuses a grid that cannot be fully
     // co-resident — the deadlock-freedom precondition of the persistent

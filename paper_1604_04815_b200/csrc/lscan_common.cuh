@@ -182,6 +182,7 @@ struct ScanParams {
     // ---- x not 16-byte aligned (scan_ws2_kernel<..., SHIFT=true>) ----
     int x_shift;                   // bytes x lies past the 16-byte boundary below it
     int head_n;                    // SHIFT: elements before x / y scanned first (y's 16-byte head)
+    int l2_resident;               // x and y together fit in L2: TMA loads evict-normal
 };
 
 // cross-GPU exchange region: [Header][parity 0: rounds x world slots][parity 1: ...]

@@ -333,7 +333,10 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
 
     if (warp == W_PROD) {
         // ------------------------------------------------------------ producer
-        const uint64_t pol = LS_TMA_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
+        // x is read once: evict-first, unless x and y fit in L2 together (the
+        // host decides, p.l2_resident), where a caller's next pass may hit it
+        const uint64_t pol =
+            (LS_TMA_EVICT_FIRST && !p.l2_resident) ? policy_evict_first() : policy_evict_normal();
         auto load_tile = [&](int64_t k) {
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
