@@ -10,6 +10,10 @@
 //     6: 256 x 16 rows (2 blocks/SM)       7: 256 x 8 rows (2 blocks/SM, product mid)
 //     8: int64 256 x 4 (product small)     9: int64 256 x 8 (product mid)
 //    10: int64 512 x 4 (2 blocks/SM)       11: int64 512 x 2
+//    12: 256 x 16 rows (1 block/SM)        13: int64 256 x 16 (1 block/SM)
+//    14: int64 256 x 12 (product large)    15: 256 x 12 (product large)
+//    16..21: 32-byte lane rows (VW = 2): 256x4, 256x8 minb2, i64 256x4, i64 256x8 minb2,
+//            i64 256x12 minb2, 256x12 minb2
 //   lab_block_elems(variant) -> elements per block (int32)
 #include <cuda_runtime.h>
 
@@ -59,7 +63,17 @@ Var var(int v) {
     case 8: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 256, 4>, 256, 4, 8};
     case 9: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 256, 2>, 256, 8, 8};
     case 10: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 512, 2>, 512, 4, 8};
-    default: return {&scan_cluster_kernel<int64_t, OpAdd, false, 2, 512, 4>, 512, 2, 8};
+    case 11: return {&scan_cluster_kernel<int64_t, OpAdd, false, 2, 512, 4>, 512, 2, 8};
+    case 12: return {&scan_cluster_kernel<int32_t, OpAdd, false, 16, 256, 1>, 256, 16};
+    case 13: return {&scan_cluster_kernel<int64_t, OpAdd, false, 16, 256, 1>, 256, 16, 8};
+    case 14: return {&scan_cluster_kernel<int64_t, OpAdd, false, 12, 256, 2>, 256, 12, 8};
+    case 15: return {&scan_cluster_kernel<int32_t, OpAdd, false, 12, 256, 2>, 256, 12};
+    case 16: return {&scan_cluster_kernel<int32_t, OpAdd, false, 4, 256, 4, 2>, 256, 4};
+    case 17: return {&scan_cluster_kernel<int32_t, OpAdd, false, 8, 256, 2, 2>, 256, 8};
+    case 18: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 256, 4, 2>, 256, 4, 8};
+    case 19: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 256, 2, 2>, 256, 8, 8};
+    case 20: return {&scan_cluster_kernel<int64_t, OpAdd, false, 12, 256, 2, 2>, 256, 12, 8};
+    default: return {&scan_cluster_kernel<int32_t, OpAdd, false, 12, 256, 2, 2>, 256, 12};
     }
 }
 }  // namespace
@@ -79,7 +93,7 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     const int C = (int)(tiles < 16 ? tiles : 16);
     const long long K = (tiles + C - 1) / C;
     if (C < 1 || (K > 1 && ((v == 4 || v == 5) || !ws))) return -1;
-    static bool init[16] = {};  // variants 0..11
+    static bool init[32] = {};  // variants 0..21
     if (!init[v]) {
         cudaFuncSetAttribute((const void *)w.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         init[v] = true;
@@ -102,6 +116,8 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = (K > 1 && coop) ? 2 : 1;
-    return (int)cudaLaunchKernelEx(&cfg, w.fn, p);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, w.fn, p);
+    if (e != cudaSuccess) (void)cudaGetLastError();  // e.g. a grid too large to be co-resident
+    return (int)e;
 }
 }

@@ -67,6 +67,19 @@ __device__ __forceinline__ void stg128_v4(void *p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
+// 256-bit global accesses (sm_100): one lane moves 32 contiguous bytes, a warp
+// a contiguous kilobyte
+__device__ __forceinline__ void ldg256(const void *p, uint4 &a, uint4 &b) {
+    asm volatile("ld.global.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ void stg256(void *p, uint4 a, uint4 b) {
+    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y),
+                 "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
 __device__ __forceinline__ uint4 ldg128(const void *p) {
     uint4 v;
     asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -76,18 +89,23 @@ __device__ __forceinline__ uint4 ldg128(const void *p) {
     return v;
 }
 
-template <typename T, typename OP, bool EXCL, int V, int THREADS, int MINB>
+// VW: 16-byte vectors per lane per row (1, or 2 for 32-byte lane chunks moved
+// by 256-bit accesses: half the warp scans per element)
+template <typename T, typename OP, bool EXCL, int V, int THREADS, int MINB, int VW = 1>
 __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanParams p) {
     constexpr int WARPS = THREADS / 32;
     constexpr int PER = 16 / (int)sizeof(T);
     constexpr int WARP_VECS = 32 * V;
     constexpr int TILE_ELEMS = WARPS * WARP_VECS * PER;
+    constexpr int VR = V / VW;       // rows per lane
+    constexpr int RPER = VW * PER;   // elements per lane per row
+    static_assert(V % VW == 0 && (VW == 1 || VW == 2), "rows of one or two vectors per lane");
     using Bits = typename Elem<T>::Bits;
     using S = Slot<T>;
 
     __shared__ T warp_tot[WARPS];
     __shared__ T warp_exc[WARPS];
-    __shared__ T row_tot[WARPS][V];       // per warp: totals of its rows
+    __shared__ T row_tot[WARPS][VR];      // per warp: totals of its rows
     __shared__ Bits cta_agg[kClusterMax];  // aggregates of the lower blocks of this cluster, stored by them
     __shared__ T block_agg;
     __shared__ T s_pre;                    // carry (+) clusters before this one (+) blocks before this one
@@ -114,25 +132,35 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     const T *x = static_cast<const T *>(p.x) + t0;
     T *y = static_cast<T *>(p.y) + t0;
     const bool xv = ((uintptr_t)x & 15u) == 0, yv = ((uintptr_t)y & 15u) == 0;
+    const bool xw = ((uintptr_t)x & 31u) == 0, yw = ((uintptr_t)y & 31u) == 0;  // 256-bit capable
     Header *hdr = reinterpret_cast<Header *>(p.ws);
     const uint32_t tag = K > 1 ? call_tag(hdr) : 0u;
 
-    // ---- load: row j of warp w is vectors w*WARP_VECS + j*32 + lane.
-    //      Whole aligned tiles take a branch-free path so all V loads are in
+    // ---- load: row j of warp w is vectors w*WARP_VECS + (j*32 + lane)*VW + u.
+    //      Whole aligned tiles take a branch-free path so all loads are in
     //      flight at once (a per-row branch makes the compiler wait on each).
     Regs<T, V> d;
     if (xv && valid == TILE_ELEMS) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) d.q[j] = ldg128(x + (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER);
+        for (int j = 0; j < VR; ++j) {
+            const T *src = x + (int64_t)(warp * WARP_VECS + (j * 32 + lane) * VW) * PER;
+            if (VW == 2 && xw) ldg256(src, d.q[2 * j], d.q[2 * j + 1]);
+            else
+#pragma unroll
+                for (int u = 0; u < VW; ++u) d.q[j * VW + u] = ldg128(src + u * PER);
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
-            if (xv && e0 + PER <= valid) {
-                d.q[j] = ldg128(x + e0);
-            } else {
+        for (int j = 0; j < VR; ++j) {
 #pragma unroll
-                for (int e = 0; e < PER; ++e) d.e[j * PER + e] = e0 + e < valid ? x[e0 + e] : ident;
+            for (int u = 0; u < VW; ++u) {
+                const int64_t e0 = (int64_t)(warp * WARP_VECS + (j * 32 + lane) * VW + u) * PER;
+                if (xv && e0 + PER <= valid) {
+                    d.q[j * VW + u] = ldg128(x + e0);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < PER; ++e) d.e[(j * VW + u) * PER + e] = e0 + e < valid ? x[e0 + e] : ident;
+                }
             }
         }
     }
@@ -140,13 +168,13 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     // ---- per row: lane-serial fold of the vector and an inclusive warp scan,
     //      then the serial row carry (Alg. 2)
     //      (row totals go to shared memory: registers are kept for the tile)
-    T rex[V];
+    T rex[VR];
     T run = ident;
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-        T v = d.e[j * PER];
+    for (int j = 0; j < VR; ++j) {
+        T v = d.e[j * RPER];
 #pragma unroll
-        for (int e = 1; e < PER; ++e) v = OP::apply(v, d.e[j * PER + e]);
+        for (int e = 1; e < RPER; ++e) v = OP::apply(v, d.e[j * RPER + e]);
         const T inc = warp_inclusive_scan<T, OP>(v, lane);
         if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code)
             rex[j] = OP::apply(inc, (T)(0 - (typename std::make_unsigned<T>::type)v));  // inc - v, exact
@@ -239,41 +267,50 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     //      serial row carry, rebuilt here to keep registers for large tiles)
     T rowpre = row_tot[warp][0];
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
+    for (int j = 0; j < VR; ++j) {
         bool has = has0;
         T acc = pre;
         if (j > 0) {
             acc = has ? OP::apply(acc, rowpre) : rowpre;
             has = true;
-            if (j + 1 < V) rowpre = OP::apply(rowpre, row_tot[warp][j]);
+            if (j + 1 < VR) rowpre = OP::apply(rowpre, row_tot[warp][j]);
         }
         if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
 #pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            const T v = d.e[j * PER + e];
+        for (int e = 0; e < RPER; ++e) {
+            const T v = d.e[j * RPER + e];
             const bool first = (e == 0 && !has);
             if (EXCL) {
-                d.e[j * PER + e] = first ? ident : acc;
+                d.e[j * RPER + e] = first ? ident : acc;
                 acc = first ? v : OP::apply(acc, v);
             } else {
                 acc = first ? v : OP::apply(acc, v);
-                d.e[j * PER + e] = acc;
+                d.e[j * RPER + e] = acc;
             }
         }
     }
     if (yv && valid == TILE_ELEMS) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) stg128_v4(y + (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER, d.q[j]);
+        for (int j = 0; j < VR; ++j) {
+            T *dst = y + (int64_t)(warp * WARP_VECS + (j * 32 + lane) * VW) * PER;
+            if (VW == 2 && yw) stg256(dst, d.q[2 * j], d.q[2 * j + 1]);
+            else
+#pragma unroll
+                for (int u = 0; u < VW; ++u) stg128_v4(dst + u * PER, d.q[j * VW + u]);
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int64_t e0 = (int64_t)(warp * WARP_VECS + j * 32 + lane) * PER;
-            if (yv && e0 + PER <= valid) {
-                stg128_v4(y + e0, d.q[j]);
-            } else {
+        for (int j = 0; j < VR; ++j) {
 #pragma unroll
-                for (int e = 0; e < PER; ++e)
-                    if (e0 + e < valid) y[e0 + e] = d.e[j * PER + e];
+            for (int u = 0; u < VW; ++u) {
+                const int64_t e0 = (int64_t)(warp * WARP_VECS + (j * 32 + lane) * VW + u) * PER;
+                if (yv && e0 + PER <= valid) {
+                    stg128_v4(y + e0, d.q[j * VW + u]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < PER; ++e)
+                        if (e0 + e < valid) y[e0 + e] = d.e[(j * VW + u) * PER + e];
+                }
             }
         }
     }

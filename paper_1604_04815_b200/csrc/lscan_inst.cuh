@@ -39,7 +39,12 @@ Launch generic_launch() {
 
 template <typename T, typename OP, bool EXCL, int V, int MINB>
 Launch cluster_launch() {
-    return {&scan_cluster_kernel<T, OP, EXCL, V, kClusterThreads, MINB>, kClusterThreads, 0,
+    // 64-bit types in the mid / large geometries: 32-byte lane rows (256-bit
+    // accesses, half the warp scans; -5-6 % per call at 2^18-2^20,
+    // profiles/r1_cluster_lab_vw.log); 32-bit and the small geometry: neutral
+    // or slower, 16-byte rows
+    constexpr int VW = (sizeof(T) == 8 && V >= 8) ? 2 : 1;
+    return {&scan_cluster_kernel<T, OP, EXCL, V, kClusterThreads, MINB, VW>, kClusterThreads, 0,
             kClusterThreads * V * 16, 1};
 }
 
