@@ -14,16 +14,23 @@ using namespace lscan;
 namespace {
 int g_lab_dtype = 0;  // ls_dtype: 0 i32, 1 i64, 2 f32, 3 f64
 
-template <int SW, int TILE, int STAGES>
+int g_lab_op = 0;     // 0 add, 1 max
+
+template <typename OP, int SW, int TILE, int STAGES, int VW>
+void (*pick())(const ScanParams) {
+    switch (g_lab_dtype) {
+    case 1: return &scan_ws2_kernel<int64_t, OP, SW, TILE, STAGES, false, false, false, VW>;
+    case 2: return &scan_ws2_kernel<float, OP, SW, TILE, STAGES, false, false, false, VW>;
+    case 3: return &scan_ws2_kernel<double, OP, SW, TILE, STAGES, false, false, false, VW>;
+    default: return &scan_ws2_kernel<int32_t, OP, SW, TILE, STAGES, false, false, false, VW>;
+    }
+}
+
+template <int SW, int TILE, int STAGES, int VW = 1>
 int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t *grid_out) {
     const bool wide = g_lab_dtype == 1 || g_lab_dtype == 3;
-    void (*f)(const ScanParams) = nullptr;
-    switch (g_lab_dtype) {
-    case 1: f = &scan_ws2_kernel<int64_t, OpAdd, SW, TILE, STAGES, false>; break;
-    case 2: f = &scan_ws2_kernel<float, OpAdd, SW, TILE, STAGES, false>; break;
-    case 3: f = &scan_ws2_kernel<double, OpAdd, SW, TILE, STAGES, false>; break;
-    default: f = &scan_ws2_kernel<int32_t, OpAdd, SW, TILE, STAGES, false>; break;
-    }
+    void (*f)(const ScanParams) =
+        g_lab_op == 1 ? pick<OpMax, SW, TILE, STAGES, VW>() : pick<OpAdd, SW, TILE, STAGES, VW>();
     const size_t smem = scan_ws2_smem_bytes<int64_t, SW, TILE, STAGES>();
     const int threads = ws2_threads<SW, false>();
     if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -64,7 +71,12 @@ extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n,
                           int64_t *grid_out) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     g_lab_dtype = (flags >> 8) & 3;
+    g_lab_op = (flags >> 10) & 1;
     switch (cfg) {
+    // 32-byte scanner rows (VW = 2) on the production geometries: 32-bit (8, 32 KiB, 6)
+    // and 64-bit (12, 48 KiB, 4)
+    case 60: return run_ws<8, 32768, 6, 2>(x, y, n, ws, s, grid_out);
+    case 61: return run_ws<12, 49152, 4, 2>(x, y, n, ws, s, grid_out);
     case 30: return run_ws<16, 32768, 4>(x, y, n, ws, s, grid_out);
     case 31: return run_ws<16, 32768, 5>(x, y, n, ws, s, grid_out);
     case 32: return run_ws<16, 32768, 6>(x, y, n, ws, s, grid_out);

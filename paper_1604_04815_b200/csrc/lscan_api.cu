@@ -7,10 +7,11 @@
 //
 // Kernel selection per call (scan_impl):
 //   n <= cluster_limit (~10 MiB), debug hooks off  -> scan_cluster_kernel (any alignment)
-//   x, y 16-byte aligned                            -> scan_ws2_kernel (TMA, persistent)
-//   x, y misaligned alike, n >= 2^20                -> generic head + ws2 on the rest
-//   x, y misaligned differently, n >= 2^20          -> ws2<SHIFT> (one launch: y's head folded
-//                                                      into the carry, shifted x windows)
+//   x 16-byte, y (16 * vw)-byte aligned             -> scan_ws2_kernel (TMA, persistent)
+//   otherwise, n >= 2^20                            -> one launch of scan_ws2_kernel (x lands
+//                                                      16-byte aligned after y's head) or of
+//                                                      ws2<SHIFT> (shifted x windows); y's head
+//                                                      folded into the carry in the kernel
 //   otherwise                                       -> scan_generic_kernel
 #include <cuda_runtime.h>
 
@@ -471,7 +472,6 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
     if ((st = device_state(&d)) != LS_OK) return st;
     const DebugCfg dbg = debug_snapshot();
 
-    const uintptr_t mx = (uintptr_t)x & 15u, my = (uintptr_t)y & 15u;
     bool launched = false;
     if (use_cluster(*d, dt, n, dbg)) {
         // a cluster grid the GPU cannot place right now (its GPCs held by
@@ -485,29 +485,22 @@ ls_status scan_impl(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, co
         }
     }
     if (!launched && st == LS_OK) {
-        if (mx == 0 && my == 0) {
+        // the persistent kernel tiles y on (16 * vw)-byte boundaries (its
+        // 256-bit stores need 32); the head before y's first boundary is folded
+        // into the carry inside the kernel, so every alignment is one launch:
+        // x then lands 16-byte aligned (TMA tiles) or not (shifted windows)
+        const unsigned ya = 16u * (unsigned)K(dt).ws2_vw[op];
+        const unsigned yoff = (unsigned)((uintptr_t)y % ya);
+        const int64_t head = yoff ? (int64_t)((ya - yoff) / (unsigned)es) : 0;
+        const uint8_t *xb = static_cast<const uint8_t *>(x) + head * es;
+        uint8_t *yb = static_cast<uint8_t *>(y) + head * es;
+        const int xs = (int)((uintptr_t)xb & 15u);
+        if (head == 0 && xs == 0) {
             st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, true, dbg);
-        } else if (mx == my && n >= kSplitMinElems) {
-            // x and y share their misalignment (e.g. a slice scanned in place):
-            // the few head elements up to the 16-byte boundary go through the
-            // generic kernel, whose total carries into the TMA kernel for the rest
-            const int64_t head = (int64_t)((16u - mx) / (unsigned)es);
-            void *scratch = static_cast<uint8_t *>(ws) + offsetof(Header, pad);
-            st = launch_scan(*d, op, dt, x, y, head, carry_in, scratch, ws, s, excl, false, dbg);
-            if (st == LS_OK)
-                st = launch_scan(*d, op, dt, static_cast<const uint8_t *>(x) + head * es,
-                                 static_cast<uint8_t *>(y) + head * es, n - head, scratch, total_out, ws, s, excl,
-                                 true, dbg);
+        } else if (n >= kSplitMinElems && xs == 0) {
+            st = launch_scan(*d, op, dt, xb, yb, n - head, carry_in, total_out, ws, s, excl, true, dbg, 0, (int)head);
         } else if (n >= kSplitMinElems && d->occ_shift[dt][op][excl] > 0) {
-            // x and y misaligned differently (e.g. a slice scanned into a fresh
-            // output): one launch of the shifted-window TMA kernel, tiled on y's
-            // 16-byte boundaries (x read through windows from the boundary below
-            // each tile); the < 16 bytes of y before its first boundary are
-            // folded into the carry inside the kernel
-            const int64_t head = my ? (int64_t)((16u - my) / (unsigned)es) : 0;
-            const uint8_t *xb = static_cast<const uint8_t *>(x) + head * es;
-            st = launch_scan(*d, op, dt, xb, static_cast<uint8_t *>(y) + head * es, n - head, carry_in, total_out, ws,
-                             s, excl, true, dbg, (int)((uintptr_t)xb & 15u), (int)head);
+            st = launch_scan(*d, op, dt, xb, yb, n - head, carry_in, total_out, ws, s, excl, true, dbg, xs, (int)head);
         } else {
             st = launch_scan(*d, op, dt, x, y, n, carry_in, total_out, ws, s, excl, false, dbg);
         }

@@ -48,6 +48,7 @@ struct Launch {
 struct DtypeKernels {
     Launch scan[kNumOps][2][2];  // [op][exclusive][fast]
     Launch multi[kNumOps][2];    // [op][exclusive]: block-cyclic multi-GPU variant of the fast kernel
+    int ws2_vw[kNumOps];         // the persistent kernel's scanner row width in vectors (y alignment 16 * vw)
     Launch shift[kNumOps][2];    // [op][exclusive]: x 16 bytes misaligned, y aligned (shifted TMA window)
     Launch cluster[kNumOps][2][kClusterGeoms];  // [op][exclusive][small, mid, large]: latency kernel (any alignment)
     const void *reduce_fn[kNumOps];

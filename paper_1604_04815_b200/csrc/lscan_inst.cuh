@@ -8,17 +8,26 @@
 
 namespace lscan {
 
+// scanner row width of the persistent kernel: 32-byte lane chunks (one
+// 256-bit store, half the warp scans) for 64-bit types and for float max/min;
+// 16-byte for the rest, where it measured neutral (profiles/r1_lab_vw.log:
+// f64 add 384 -> 410, f32 max 570 -> 592, i64 add +1 %, 32-bit add +-0)
+template <typename T, typename OP>
+constexpr int ws2_vw() {
+    return (sizeof(T) == 8 || order_sensitive<T, OP>()) ? 2 : 1;
+}
+
 template <typename T, typename OP, bool EXCL>
 Launch fast_launch() {
     using C = FastCfg<sizeof(T)>;
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL>, ws2_threads<C::kScanWarps, false>(),
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, false, ws2_vw<T, OP>()>, ws2_threads<C::kScanWarps, false>(),
             scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(), C::kTileBytes, C::kStages};
 }
 
 template <typename T, typename OP, bool EXCL>
 Launch shift_launch() {
     using C = FastCfg<sizeof(T)>;
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true>,
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true, ws2_vw<T, OP>()>,
             ws2_threads<C::kScanWarps, false>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true>(),
             C::kTileBytes, C::kStages};
 }
@@ -26,7 +35,7 @@ Launch shift_launch() {
 template <typename T, typename OP, bool EXCL>
 Launch multi_launch() {
     using C = MultiCfg<sizeof(T)>;
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true>,
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true, false, ws2_vw<T, OP>()>,
             ws2_threads<C::kScanWarps, true>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(),
             C::kTileBytes, C::kStages};
 }
@@ -62,6 +71,7 @@ void fill_op(DtypeKernels &k) {
     k.scan[OP::code][1][0] = generic_launch<T, OP, true>();
     k.multi[OP::code][0] = multi_launch<T, OP, false>();
     k.multi[OP::code][1] = multi_launch<T, OP, true>();
+    k.ws2_vw[OP::code] = ws2_vw<T, OP>();
     k.shift[OP::code][0] = shift_launch<T, OP, false>();
     k.shift[OP::code][1] = shift_launch<T, OP, true>();
     k.reduce_fn[OP::code] = (const void *)&reduce_kernel<T, OP, kReduceThreads>;

@@ -266,14 +266,20 @@ __device__ __forceinline__ uint64_t *xchg_slots(uint8_t *region, uint32_t xtag, 
            (int64_t)(xtag & 1u) * rounds_cap * world * Slot<T>::W;
 }
 
+// VW: 16-byte vectors per lane per scanner row (1, or 2: 32-byte lane chunks,
+// one 256-bit store each, half the warp scans per element)
 template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL, bool MULTI = false,
-          bool SHIFT = false>
+          bool SHIFT = false, int VW = 1>
 __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_kernel(const ScanParams p) {
     constexpr int SCAN_THREADS = SCAN_WARPS * 32;
     constexpr int V = TILE_BYTES / SCAN_THREADS / 16;  // rows (16-byte vectors) per lane
     constexpr int PER = 16 / (int)sizeof(T);           // elements per vector
     constexpr int TILE_ELEMS = TILE_BYTES / (int)sizeof(T);
     constexpr int WARP_BYTES = TILE_BYTES / SCAN_WARPS;
+    constexpr int VR = V / VW;      // scanner rows per lane
+    constexpr int RPER = VW * PER;  // elements per lane per row
+    constexpr uint32_t ROW_BYTES = 512u * VW;
+    static_assert(V % VW == 0 && (VW == 1 || VW == 2), "rows of one or two vectors per lane");
     constexpr int W_PROD = SCAN_WARPS, W_RED = SCAN_WARPS + 1, W_AUX = SCAN_WARPS + 2;
     constexpr int W_PUSH = SCAN_WARPS + 3, W_GCHAIN = SCAN_WARPS + 4;  // MULTI only, CTA G-1 only
     static_assert(V >= 1 && TILE_BYTES % (SCAN_THREADS * 16) == 0, "whole rows per lane");
@@ -451,17 +457,14 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
         const T *carry_in = static_cast<const T *>(p.carry_in);
         bool have_carry = carry_in != nullptr;
         T r_prev = have_carry ? *carry_in : ident;  // R[k-1] as known to CTA G-1 (the chain owner)
-        if constexpr (SHIFT) {
-            // y's head (the < 16 bytes before the aligned y this kernel tiles):
-            // every CTA folds it into the carry, in sequence order; CTA 0
-            // stores it.  One launch for any alignment
+        if constexpr (!MULTI) {
+            // y's head (the few elements before the aligned y this kernel
+            // tiles): every CTA folds it into the carry, in sequence order;
+            // the last CTA to finish stores it (below), after every CTA has
+            // read it — so x == y is safe.  One launch for any alignment
             const T *hx = x - p.head_n;
-            T *hy = y - p.head_n;
             for (int i = 0; i < p.head_n; ++i) {
-                const T v = hx[i];
-                const T before = r_prev;
-                r_prev = have_carry ? OP::apply(r_prev, v) : v;
-                if (c == 0 && lane == 0) hy[i] = EXCL ? (have_carry ? before : ident) : r_prev;
+                r_prev = have_carry ? OP::apply(r_prev, hx[i]) : hx[i];
                 have_carry = true;
             }
         }
@@ -580,7 +583,8 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
         }
     } else if (warp < SCAN_WARPS) {
         // ------------------------------------------------------------ scanners
-        const uint32_t wbase = (uint32_t)warp * WARP_BYTES + (uint32_t)lane * 16;  // row 0 of this lane
+        const uint32_t wbase = (uint32_t)warp * WARP_BYTES + (uint32_t)lane * 16u * VW;  // row 0 of this lane
+        const bool y256 = VW == 2 && ((uintptr_t)y & 31u) == 0;
         for (int64_t k = 0; k < my_tiles; ++k) {
             const int s = (int)(k % STAGES);
             const uint32_t parity = (uint32_t)((k / STAGES) & 1);
@@ -597,21 +601,29 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                 // a whole number of 32-bit words)
                 const int sw = p.x_shift >> 2;
 #pragma unroll
-                for (int j = 0; j < V; ++j)
-                    r.q[j] = funnel_words(lds128(sbase + (uint32_t)j * 512u), lds128(sbase + (uint32_t)j * 512u + 16u),
-                                          sw);
+                for (int j = 0; j < VR; ++j) {
+                    uint4 a = lds128(sbase + (uint32_t)j * ROW_BYTES);
+#pragma unroll
+                    for (int u = 0; u < VW; ++u) {
+                        const uint4 b = lds128(sbase + (uint32_t)j * ROW_BYTES + 16u * (u + 1));
+                        r.q[j * VW + u] = funnel_words(a, b, sw);
+                        a = b;
+                    }
+                }
             } else {
 #pragma unroll
-                for (int j = 0; j < V; ++j) r.q[j] = lds128(sbase + (uint32_t)j * 512u);
+                for (int j = 0; j < VR; ++j)
+#pragma unroll
+                    for (int u = 0; u < VW; ++u) r.q[j * VW + u] = lds128(sbase + (uint32_t)j * ROW_BYTES + 16u * u);
             }
-            // per row j: lane-serial fold of the vector, inclusive warp scan
-            T rex[V];   // exclusive prefix of this lane within row j (lane > 0)
-            T rtot[V];  // row totals
+            // per row j: lane-serial fold of the lane's chunk, inclusive warp scan
+            T rex[VR];   // exclusive prefix of this lane within row j (lane > 0)
+            T rtot[VR];  // row totals
 #pragma unroll
-            for (int j = 0; j < V; ++j) {
-                T v = r.e[j * PER];
+            for (int j = 0; j < VR; ++j) {
+                T v = r.e[j * RPER];
 #pragma unroll
-                for (int e = 1; e < PER; ++e) v = OP::apply(v, r.e[j * PER + e]);
+                for (int e = 1; e < RPER; ++e) v = OP::apply(v, r.e[j * RPER + e]);
                 if (LS_LAB_SKIP_ROWSCAN) {
                     rex[j] = v;
                     rtot[j] = v;
@@ -630,7 +642,7 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             // serial row carry (Alg. 2): the warp's total over its rows
             T run = rtot[0];
 #pragma unroll
-            for (int j = 1; j < V; ++j) run = OP::apply(run, rtot[j]);
+            for (int j = 1; j < VR; ++j) run = OP::apply(run, rtot[j]);
             if (lane == 0) warp_tot[warp] = run;
             named_bar_sync(1, SCAN_THREADS);  // (A) stage fully read; warp totals visible
             long long tm2 = LS_LAB_TIMING ? clock64() : 0;
@@ -664,34 +676,43 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             // the warp total above; no per-row array kept across the wait)
             T rowpre = rtot[0];
 #pragma unroll
-            for (int j = 0; j < V; ++j) {
+            for (int j = 0; j < VR; ++j) {
                 bool has = has0;
                 T acc = wcarry;
                 if (j > 0) {
                     acc = has ? OP::apply(acc, rowpre) : rowpre;
                     has = true;
-                    if (j + 1 < V) rowpre = OP::apply(rowpre, rtot[j]);
+                    if (j + 1 < VR) rowpre = OP::apply(rowpre, rtot[j]);
                 }
                 if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
 #pragma unroll
-                for (int e = 0; e < PER; ++e) {
-                    const T v = r.e[j * PER + e];
+                for (int e = 0; e < RPER; ++e) {
+                    const T v = r.e[j * RPER + e];
                     const bool first = (e == 0 && !has);
                     if (EXCL) {
-                        r.e[j * PER + e] = first ? ident : acc;
+                        r.e[j * RPER + e] = first ? ident : acc;
                         acc = first ? v : OP::apply(acc, v);
                     } else {
                         acc = first ? v : OP::apply(acc, v);
-                        r.e[j * PER + e] = acc;
+                        r.e[j * RPER + e] = acc;
                     }
                 }
-                const int64_t vec = (int64_t)warp * (WARP_BYTES / 16) + j * 32 + lane;  // 16-byte vector index
-                if (!partial || (vec + 1) * PER <= valid) {
-                    stg128(reinterpret_cast<uint8_t *>(yt) + vec * 16, r.q[j]);
-                } else if (vec * PER < valid) {
+                // 16-byte vector index of the lane's chunk in this row
+                const int64_t vec = (int64_t)warp * (WARP_BYTES / 16) + (int64_t)(j * 32 + lane) * VW;
+                if (VW == 2 && y256 && (!partial || (vec + 2) * PER <= valid)) {
+                    stg256(reinterpret_cast<uint8_t *>(yt) + vec * 16, r.q[j * VW], r.q[j * VW + 1]);
+                } else {
 #pragma unroll
-                    for (int e = 0; e < PER; ++e)
-                        if (vec * PER + e < valid) yt[vec * PER + e] = r.e[j * PER + e];
+                    for (int u = 0; u < VW; ++u) {
+                        const int64_t vu = vec + u;
+                        if (!partial || (vu + 1) * PER <= valid) {
+                            stg128(reinterpret_cast<uint8_t *>(yt) + vu * 16, r.q[j * VW + u]);
+                        } else if (vu * PER < valid) {
+#pragma unroll
+                            for (int e = 0; e < PER; ++e)
+                                if (vu * PER + e < valid) yt[vu * PER + e] = r.e[(j * VW + u) * PER + e];
+                        }
+                    }
                 }
             }
             if (LS_LAB_TIMING && tid == 0) {
@@ -727,7 +748,24 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
                 st_relaxed_u32(&hdr->epoch, tag);
             }
         } else {
-            epoch_handover(hdr, tag, G);
+            const uint32_t old = atom_add_acqrel_u32(&hdr->done, 1u);
+            if (old == (uint32_t)G - 1u) {
+                // every CTA has finished (and read y's head): store the head
+                const T *hx = x - p.head_n;
+                T *hy = y - p.head_n;
+                const T *cin = static_cast<const T *>(p.carry_in);
+                bool has = cin != nullptr;
+                T acc = has ? *cin : ident;
+                for (int i = 0; i < p.head_n; ++i) {
+                    const T v = hx[i];
+                    const T before = acc;
+                    acc = has ? OP::apply(acc, v) : v;
+                    hy[i] = EXCL ? (has ? before : ident) : acc;
+                    has = true;
+                }
+                st_relaxed_u32(&hdr->done, 0u);
+                st_relaxed_u32(&hdr->epoch, tag);
+            }
         }
     }
 }

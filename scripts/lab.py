@@ -24,7 +24,7 @@ CFG_NAMES = {30: "reg16/32K/4", 31: "reg16/32K/5", 32: "reg16/32K/6", 33: "reg16
              35: "reg16/64K/3", 36: "reg16/16K/12", 37: "reg8/16K/12", 38: "reg24/48K/4", 40: "reg12/48K/4",
              41: "reg8/32K/5", 42: "reg8/32K/4", 43: "reg12/48K/3", 44: "reg16/64K/3", 45: "reg4/32K/6",
              46: "reg8/16K/4", 47: "reg4/16K/4", 48: "reg8/16K/3", 49: "reg4/8K/4", 50: "reg8/32K/2",
-             51: "reg4/16K/2"}
+             51: "reg4/16K/2", 60: "reg8/32K/6/vw2", 61: "reg12/48K/4/vw2"}
 
 
 def timeit(fn, reps, warm=3):
@@ -76,6 +76,7 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--wide", action="store_true", help="64-bit elements (same as --dtype i64)")
     ap.add_argument("--dtype", choices=["i32", "i64", "f32", "f64"], default=None)
+    ap.add_argument("--op", choices=["add", "max"], default="add")
     ap.add_argument("--labso", default="liblscanlab.so", help="lab library in bench_support/_build")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (device time, no host)")
     ap.add_argument("--product", action="store_true", help="also time the product call (scan.inclusive_scan)")
@@ -102,13 +103,16 @@ def main():
     ws = torch.zeros(L.ls_workspace_bytes(N.LS_I64, n) * 8, dtype=torch.uint8, device="cuda")
     g = ctypes.c_int64(0)
     ref = torch.cumsum(x, 0, dtype=dt) if not dt.is_floating_point else torch.cumsum(x.double(), 0)
+    if args.op == "max":
+        ref = torch.cummax(x, 0).values
+    flags = (code << 8) | ((1 << 10) if args.op == "max" else 0)
     res = {"n": n, "dtype": str(dt), "lib": args.labso}
     res["torch_copy_gbs"] = round(2 * n * es / (timeit(lambda: y.copy_(x), args.reps) * 1e-3) / 1e9, 1)
     res["torch_cumsum_gelems"] = round(n / (timeit(lambda: torch.cumsum(x, 0, dtype=dt, out=y),
                                                    args.reps) * 1e-3) * 1e-9, 1)
     for cfg in [int(c) for c in args.cfgs.split(",")]:
         def step():
-            rc = LAB.ls_lab_run(cfg, code << 8, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(),
+            rc = LAB.ls_lab_run(cfg, flags, x.data_ptr(), y.data_ptr(), n, ws.data_ptr(),
                                 torch.cuda.current_stream().cuda_stream, ctypes.byref(g))
             assert rc == 0, rc
         if args.sustain:
@@ -136,13 +140,13 @@ def main():
         res[f"cfg{cfg}_{CFG_NAMES[cfg]}"] = {
             "gelems": round(n / (ms * 1e-3) * 1e-9, 1), "gbs": round(2 * n * es / (ms * 1e-3) / 1e9, 1),
             "grid": g.value,
-            "ok": bool(torch.equal(y, ref)) if not dt.is_floating_point
+            "ok": bool(torch.equal(y, ref)) if (not dt.is_floating_point or args.op == "max")
             else bool(((y.double() - ref).abs() <= 1e-4 * torch.cumsum(x.double().abs(), 0)).all())}
     if args.product:
         from paper_1604_04815_b200 import scan as S
 
         def prod():
-            S.inclusive_scan(x, out=y)
+            S.inclusive_scan(x, out=y, op=args.op)
         ms = graph_ms(prod, args.reps) if args.graph else timeit(prod, args.reps)
         res["product"] = {"gelems": round(n / (ms * 1e-3) * 1e-9, 1), "us": round(ms * 1e3, 2)}
     print(json.dumps(res, indent=None if args.graph else 1))

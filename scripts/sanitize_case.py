@@ -41,6 +41,13 @@ for dt in (torch.int32, torch.float64):
             yb = torch.empty(n + 1, dtype=dt, device="cuda")
             S.inclusive_scan(x, out=yb[1:], op="max")
             assert torch.equal(yb[1:], torch.cummax(x, 0).values), (dt, n, "shifted max")
+            # congruent slices in place (x == y, head stored by the last CTA)
+            # and y 16 bytes past a 32-byte boundary
+            for off in (1, 16 // x.element_size()):
+                z = ((torch.arange(n + off, dtype=dt, device="cuda") % 7) - 3)
+                ref = torch.cumsum(z[off:].double(), 0).to(dt)
+                S.inclusive_scan(z[off:], out=z[off:])
+                assert torch.equal(z[off:], ref), (dt, n, "in place", off)
     if mode in ("cluster", "shifted"):
         continue
     tile = S.query_config(dt, 1 << 20)["tile_elems"]
