@@ -9,12 +9,12 @@
 namespace lscan {
 
 // scanner row width of the persistent kernel: 32-byte lane chunks (one
-// 256-bit store, half the warp scans) for 64-bit types and for float max/min;
-// 16-byte for the rest, where it measured neutral (profiles/r1_lab_vw.log:
-// f64 add 384 -> 410, f32 max 570 -> 592, i64 add +1 %, 32-bit add +-0)
+// 256-bit store, half the warp scans) for every type and operator
+// (profiles/r1_lab_vw.log: f64 add 384 -> 410, f32 max 570 -> 592, i64 add
+// +1 %, 32-bit add +-0 burst and +1.3 % under sustained load)
 template <typename T, typename OP>
 constexpr int ws2_vw() {
-    return (sizeof(T) == 8 || order_sensitive<T, OP>()) ? 2 : 1;
+    return 2;
 }
 
 template <typename T, typename OP, bool EXCL>
