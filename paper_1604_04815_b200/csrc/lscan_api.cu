@@ -80,7 +80,8 @@ ls_status cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
 
-// below this size a misaligned input stays on the generic kernel (one launch)
+// below this size a misaligned input the latency kernel does not take (debug
+// hooks armed, forced persistent path) runs on the generic kernel
 constexpr int64_t kSplitMinElems = 1 << 20;
 
 // LSCAN_NO_COOP=1: plain launches (lab measurement of the cooperative-launch

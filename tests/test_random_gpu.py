@@ -3,7 +3,7 @@ y offset, in place, carry, kernel choice) and every draw is checked against
 the oracle — ints and max/min bit-exact, float add within the reference
 envelope (bench.py:49, :90-114).  Sizes span every kernel's regime (one
 cluster, several clusters, the persistent chain) and every alignment case
-(aligned TMA path, congruent split, generic)."""
+(aligned TMA path, in-kernel head + TMA or shifted-window path, generic)."""
 
 import numpy as np
 import pytest

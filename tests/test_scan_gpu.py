@@ -159,8 +159,8 @@ def test_misaligned_generic_path(S1, oracle_lib, tok):
 @pytest.mark.parametrize("shift", [1, 2, 3])
 def test_congruent_misalignment_split_path(S1, oracle_lib, tok, shift):
     # x and y misaligned by the same amount (a slice scanned in place, or two
-    # slices at equal offsets): head elements on the generic kernel, the rest
-    # on the TMA kernel with the head's total as carry
+    # slices at equal offsets): one TMA-kernel launch over the aligned body,
+    # y's head folded into the carry in the kernel and stored by its last CTA
     es = 4 if tok in ("i32", "f32") else 8
     if (shift * es) % 16 == 0:
         pytest.skip("aligned")

@@ -108,8 +108,8 @@ def test_ties_reduce(S, tok, op, kind, n):
 @pytest.mark.parametrize("kind", ["dense_zeros", "sparse_zeros", "nans"])
 @pytest.mark.parametrize("xoff,yoff", [(1, 0), (0, 1), (3, 2)])
 def test_ties_misaligned(S, tok, op, kind, xoff, yoff):
-    """The shifted-window path (x and y misaligned differently): generic head,
-    shifted tiles, latency-kernel tail, totals carried between them."""
+    """x and y misaligned differently: one launch — y's head folded into the
+    carry in the kernel, x through shifted TMA windows, the ragged end bounded."""
     n = (1 << 21) + 5
     x = make(kind, tok, op, n, 5)
     xb = torch.empty(n + 4, dtype=TDT[tok], device="cuda")
