@@ -14,6 +14,7 @@
 //    14: int64 256 x 12 (product large)    15: 256 x 12 (product large)
 //    16..21: 32-byte lane rows (VW = 2): 256x4, 256x8 minb2, i64 256x4, i64 256x8 minb2,
 //            i64 256x12 minb2, 256x12 minb2
+//    22..24: i64, 512 threads, VW = 2: 4 rows minb2, 8 rows minb1, 6 rows minb1
 //   lab_block_elems(variant) -> elements per block (int32)
 #include <cuda_runtime.h>
 
@@ -73,7 +74,10 @@ Var var(int v) {
     case 18: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 256, 4, 2>, 256, 4, 8};
     case 19: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 256, 2, 2>, 256, 8, 8};
     case 20: return {&scan_cluster_kernel<int64_t, OpAdd, false, 12, 256, 2, 2>, 256, 12, 8};
-    default: return {&scan_cluster_kernel<int32_t, OpAdd, false, 12, 256, 2, 2>, 256, 12};
+    case 21: return {&scan_cluster_kernel<int32_t, OpAdd, false, 12, 256, 2, 2>, 256, 12};
+    case 22: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 512, 2, 2>, 512, 4, 8};
+    case 23: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 512, 1, 2>, 512, 8, 8};
+    default: return {&scan_cluster_kernel<int64_t, OpAdd, false, 6, 512, 1, 2>, 512, 6, 8};
     }
 }
 }  // namespace

@@ -19,8 +19,9 @@ NAMES = {0: "scan_256x4", 1: "scan_512x4", 2: "scan_256x8", 3: "scan_256x2", 4: 
          6: "scan_256x16_minb2", 7: "scan_256x8_minb2", 8: "i64_256x4", 9: "i64_256x8_minb2",
          10: "i64_512x4_minb2", 11: "i64_512x2", 12: "scan_256x16_minb1", 13: "i64_256x16_minb1",
          14: "i64_256x12_minb2", 15: "scan_256x12_minb2", 16: "vw2_256x4", 17: "vw2_256x8_minb2",
-         18: "vw2_i64_256x4", 19: "vw2_i64_256x8_minb2", 20: "vw2_i64_256x12_minb2", 21: "vw2_256x12_minb2"}
-WIDE = {8, 9, 10, 11, 13, 14, 18, 19, 20}
+         18: "vw2_i64_256x4", 19: "vw2_i64_256x8_minb2", 20: "vw2_i64_256x12_minb2", 21: "vw2_256x12_minb2",
+         22: "vw2_i64_512x4_minb2", 23: "vw2_i64_512x8_minb1", 24: "vw2_i64_512x6_minb1"}
+WIDE = {8, 9, 10, 11, 13, 14, 18, 19, 20, 22, 23, 24}
 
 
 def main():
