@@ -405,7 +405,17 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
     const Launch &L = x_shift ? K(dt).shift[op][excl] : K(dt).scan[op][excl][fast];
     const int64_t M = num_tiles(dt, n, fast);
     const int64_t cap = (int64_t)(x_shift ? d.occ_shift[dt][op][excl] : d.occ[dt][op][excl][fast]) * d.sms;
-    const int G = (int)std::min<int64_t>(M, cap);
+    int G = (int)std::min<int64_t>(M, cap);
+    static const int balanced = [] {
+        const char *e = getenv("LSCAN_BALANCED_GRID");  // lab switch
+        return e ? atoi(e) : 0;
+    }();
+    if (balanced && G > 0) {
+        // the fewest CTAs that keep the same number of rounds: every CTA gets
+        // the same tile count
+        const int64_t rounds = (M + G - 1) / G;
+        G = (int)((M + rounds - 1) / rounds);
+    }
     ScanParams p{};
     p.x = x;
     p.y = y;
