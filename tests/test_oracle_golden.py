@@ -6,6 +6,7 @@ restatements in oracle/ against them.  CPU only.
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -201,3 +202,17 @@ def test_float_max_min_tie_semantics(oracle_lib, dt):
     for op in ("max", "min"):
         y = oracle_lib.sequential_scan(x, op=op)
         assert not np.isnan(y[0]) and np.isnan(y[1:]).all() and np.signbit(y[1:]).all(), op
+
+
+def test_ties_oracle_matches_reference(oracle_lib):
+    """tests/golden/ties_cases.npz: float max/min over signed-zero mixes and NaN
+    payloads, computed by the real reference (sequential_scan and its threaded
+    chained_scan agree bit for bit) — the oracle restates them exactly."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "ties_cases.npz"))
+    keys = sorted(k[2:] for k in z.files if k.startswith("x_"))
+    assert len(keys) == 24
+    for key in keys:
+        name = key.split("_")[0]
+        x, ref = z["x_" + key], z["seq_" + key]
+        got = oracle_lib.sequential_scan(x, op=name)
+        assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), key

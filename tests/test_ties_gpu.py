@@ -121,3 +121,26 @@ def test_ties_misaligned(S, tok, op, kind, xoff, yoff):
     ref = seq(x, op)
     assert np.array_equal(yd.cpu().numpy().view(UI[tok]), ref.view(UI[tok]))
     assert tot.cpu().numpy().view(UI[tok])[0] == ref[-1:].view(UI[tok])[0]
+
+
+@pytest.fixture(scope="module")
+def ties_golden():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "ties_cases.npz"))
+
+
+@pytest.mark.parametrize("path", ["auto", "persistent"])
+@pytest.mark.parametrize("excl", [False, True])
+def test_ties_match_reference_fixtures(S, ties_golden, path, excl):
+    """The CUDA scan against the reference's own outputs (tests/golden/
+    make_ties_golden.py), bit for bit, on the latency and persistent kernels."""
+    keys = sorted(k[2:] for k in ties_golden.files if k.startswith("x_"))
+    for key in keys:
+        name, tok = key.split("_")[0], key.split("_")[1]
+        x, ref = ties_golden["x_" + key], ties_golden["seq_" + key]
+        fn = S.exclusive_scan if excl else S.inclusive_scan
+        with S.force_path(path):
+            y = fn(torch.from_numpy(x).cuda(), op=name).cpu().numpy()
+        if excl:
+            ref = np.concatenate([[-np.inf if name == "max" else np.inf], ref[:-1]]).astype(x.dtype)
+        assert np.array_equal(y.view(UI[tok]), ref.view(UI[tok])), (key, path, excl)
