@@ -46,7 +46,10 @@ typedef enum { LS_I32 = 0, LS_I64 = 1, LS_F32 = 2, LS_F64 = 3 } ls_dtype;
 
 /* Scan operators (make_operator, operators.py:111-127): add (identity 0,
  * integers wrap), max (identity = lowest value / -inf), min (highest / +inf).
- * Float max/min propagate NaN like numpy.maximum / numpy.minimum. */
+ * Float max/min are bit-exact to numpy.maximum / numpy.minimum.accumulate,
+ * tie rules included: maximum(a, b) = (a > b || isnan(a)) ? a : b, so equal
+ * operands give the right one (the sign of a zero result is the rightmost
+ * maximal zero's) and a NaN propagates as the leftmost NaN's bits. */
 typedef enum { LS_OP_ADD = 0, LS_OP_MAX = 1, LS_OP_MIN = 2 } ls_op;
 
 /* ---- workspace ------------------------------------------------------------
@@ -66,6 +69,10 @@ ls_status ls_workspace_init(void *ws, size_t ws_bytes, void *stream);
  *   carry from lower shards.
  * total_out: nullable device scalar receiving carry (+) x[0] (+) ... (+) x[n-1];
  *   must not alias carry_in.
+ * Any element alignment of x and y: 16-byte aligned x with 32-byte aligned y
+ * runs at the HBM roofline; other alignments are still one launch (the few
+ * elements before y's boundary are folded into the carry inside the kernel,
+ * a misaligned x is read through shifted TMA windows) at 84-101 %.
  * Replaces chained_scan (chained.py:316) for the given operator. */
 ls_status ls_inclusive_scan(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
                             const void *carry_in, void *total_out,
