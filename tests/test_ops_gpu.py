@@ -97,3 +97,25 @@ def test_dropin_c1_max(oracle_lib):
     op = P.make_operator("min", "f64")
     x = oracle_lib.generate_input(50_000_003, "f64", [0, 1])
     assert bits_equal(P.chained_scan(P.ScanProblem(x, op)), oracle_lib.sequential_scan(x, op="min"))
+
+
+@pytest.mark.parametrize("tok", TOKS)
+@pytest.mark.parametrize("name", ["add", "max", "min"])
+def test_reduce_misaligned_slices(S, oracle_lib, tok, name):
+    """ls_reduce over slices at every element offset (the reduction's
+    16-byte head, vector body and ragged tail), sizes from one element to
+    several grid strides; ints and max/min exact, float add in the envelope."""
+    dt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[tok]
+    for n in (1, 3, 17, 1000, 65_537, 3_000_001):
+        base = oracle_lib.generate_input(n + 4, tok, [11, n])
+        xd = torch.from_numpy(base).cuda()
+        for off in range(4):
+            x = base[off:off + n]
+            got = S.reduce(xd[off:off + n], op=name).cpu().numpy().reshape(-1)[0]
+            if tok[0] == "i" or name != "add":
+                want = oracle_lib.sequential_scan(x, op=name)[-1]
+                assert bits_equal(np.array([got]), np.array([want])), (n, off)
+            else:
+                want = np.add.reduce(x.astype(np.float64))
+                env = oracle_lib.FLOAT_EPS_REL[tok] * np.abs(x.astype(np.float64)).sum() * 4 + 1e-30
+                assert abs(float(got) - want) <= env, (n, off, got, want)
