@@ -49,6 +49,7 @@ struct Elem<double> {
 struct OpAdd {
     static constexpr int code = 0;
     static constexpr bool idempotent = false;
+    static constexpr bool three = false;  // no three-input form (apply3)
     template <typename T>
     __device__ __forceinline__ static T apply(T a, T b) {
         if constexpr (std::is_integral<T>::value) {
@@ -92,6 +93,7 @@ __device__ __forceinline__ T float_keep_a(T a, T b) {
 struct OpMax {
     static constexpr int code = 1;
     static constexpr bool idempotent = true;  // x (+) x == x, bit for bit
+    static constexpr bool three = false;
     template <typename T>
     __device__ __forceinline__ static T apply(T a, T b) {
         if constexpr (std::is_integral<T>::value) {
@@ -111,6 +113,7 @@ struct OpMax {
 struct OpMin {
     static constexpr int code = 2;
     static constexpr bool idempotent = true;
+    static constexpr bool three = false;
     template <typename T>
     __device__ __forceinline__ static T apply(T a, T b) {
         if constexpr (std::is_integral<T>::value) {
@@ -329,6 +332,79 @@ __device__ __forceinline__ T warp_inclusive_scan(T v, int lane) {
     }
     return v;
 }
+
+// f32 max / min as one FMNMX: identical to numpy's maximum / minimum on
+// operands that are neither zeros nor NaNs (no two distinct bit patterns
+// compare equal there, and no NaN to propagate).  The persistent kernel's
+// scanners use it for a warp's chunk of a tile holding no zero and no NaN.
+// apply3: the three-input FMNMX3 (sm_100) for folds of a lane's elements.
+struct OpFastMaxF {
+    static constexpr int code = 1;
+    static constexpr bool idempotent = true;
+    static constexpr bool three = true;
+    __device__ __forceinline__ static float apply(float a, float b) { return fmaxf(a, b); }
+    __device__ __forceinline__ static float apply3(float a, float b, float c) {
+        float r;
+        asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+        return r;
+    }
+};
+struct OpFastMinF {
+    static constexpr int code = 2;
+    static constexpr bool idempotent = true;
+    static constexpr bool three = true;
+    __device__ __forceinline__ static float apply(float a, float b) { return fminf(a, b); }
+    __device__ __forceinline__ static float apply3(float a, float b, float c) {
+        float r;
+        asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+        return r;
+    }
+};
+// The reducers' f32 max / min: NaN-propagating FMNMX(3).NAN — any NaN makes
+// the result a NaN, otherwise it is exact up to the sign of a zero; both
+// cases are then re-derived exactly (tile_ties).  Commutative, so lanes agree.
+struct OpNanMaxF {
+    __device__ __forceinline__ static float apply(float a, float b) {
+        float r;
+        asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+        return r;
+    }
+    __device__ __forceinline__ static float apply3(float a, float b, float c) {
+        float r;
+        asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+        return r;
+    }
+};
+struct OpNanMinF {
+    __device__ __forceinline__ static float apply(float a, float b) {
+        float r;
+        asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+        return r;
+    }
+    __device__ __forceinline__ static float apply3(float a, float b, float c) {
+        float r;
+        asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+        return r;
+    }
+};
+
+template <typename T, typename OP>
+struct ScanFastOp {
+    static constexpr bool enabled = false;
+    using type = OP;
+};
+template <>
+struct ScanFastOp<float, struct OpMax> {
+    static constexpr bool enabled = true;
+    using type = OpFastMaxF;
+    using reduce_type = OpNanMaxF;
+};
+template <>
+struct ScanFastOp<float, struct OpMin> {
+    static constexpr bool enabled = true;
+    using type = OpFastMinF;
+    using reduce_type = OpNanMinF;
+};
 
 // Float max/min results depend on the ORDER of equal-comparing operands (-0 /
 // +0) and of NaNs: the sequential fold yields the rightmost of the maximal

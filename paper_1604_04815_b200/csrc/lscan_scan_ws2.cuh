@@ -90,11 +90,49 @@ __device__ __noinline__ T tile_ties(const uint8_t *st, int lane, T fast, int nve
 
 // reduce a whole shared-memory tile with one warp (lane-strided 16-byte
 // vectors, conflict-free), four independent accumulators, fixed order
+// f32 max / min: the whole tile with FMNMX3.NAN (two elements per operator,
+// no NaN or sign-of-zero bookkeeping), then the exact re-derivation when the
+// result is a NaN or a zero.  Window elements outside [lo, hi) are skipped
+// (identity).
+template <typename T, typename OP, int NVEC>
+__device__ __forceinline__ T reduce_stage_nan(const uint8_t *st, int lane, int lo, int hi) {
+    using R = typename ScanFastOp<T, OP>::reduce_type;
+    const T ident = OP::template identity<T>();
+    T acc[4] = {ident, ident, ident, ident};
+    const uint32_t base = smem_u32(st);
+    constexpr int ITERS = (NVEC + 31) / 32;  // lane-strided vectors per lane
+#pragma unroll 2
+    for (int i = 0; i < ITERS; i += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // four independent chains
+            const int v = (i + u) * 32 + lane;
+            if (v < NVEC) {
+                Regs<T, 1> r;
+                r.q[0] = lds128(base + (uint32_t)v * 16u);
+                if (v * 4 < lo || v * 4 + 4 > hi) {  // the window's edge vectors only
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (v * 4 + e < lo || v * 4 + e >= hi) r.e[e] = ident;
+                }
+                acc[u] = R::apply3(acc[u], r.e[0], r.e[1]);
+                acc[u] = R::apply3(acc[u], r.e[2], r.e[3]);
+            }
+        }
+    }
+    T x = R::apply(R::apply3(acc[0], acc[1], acc[2]), acc[3]);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) x = R::apply(x, __shfl_xor_sync(0xffffffffu, x, d));
+    if (tie_class(x)) return tile_ties<T, OP>(st, lane, x, NVEC, lo, hi);
+    return x;
+}
+
 template <typename T, typename OP, int TILE_BYTES>
 __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
     constexpr int NV = TILE_BYTES / 16 / 32;  // 16-byte vectors per lane
     constexpr int PER = 16 / (int)sizeof(T);
     static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
+    if constexpr (ScanFastOp<T, OP>::enabled)
+        return reduce_stage_nan<T, OP, TILE_BYTES / 16>(st, lane, 0, TILE_BYTES / (int)sizeof(T));
     const T ident = OP::template identity<T>();
     T acc[4] = {ident, ident, ident, ident};
     const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
@@ -123,6 +161,8 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
     constexpr int NV = TILE_BYTES / 16 / 32;
     constexpr int PER = 16 / (int)sizeof(T);
     static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
+    if constexpr (ScanFastOp<T, OP>::enabled)
+        return reduce_stage_nan<T, OP, TILE_BYTES / 16 + 1>(st, lane, sh, sh + TILE_BYTES / (int)sizeof(T));
     const T ident = OP::template identity<T>();
     T acc[4] = {ident, ident, ident, ident};
     const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
@@ -616,33 +656,64 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
 #pragma unroll
                     for (int u = 0; u < VW; ++u) r.q[j * VW + u] = lds128(sbase + (uint32_t)j * ROW_BYTES + 16u * u);
             }
+            // f32 max / min: a warp chunk with no zero and no NaN scans with
+            // one FMNMX per operator (ScanFastOp).  u = 2 * bits - 1 (one
+            // IADD3) is 0xffffffff for +-0 and above 0xff000000 for a NaN,
+            // at most 0xfeffffff otherwise (infinities included)
+            bool fast = false;
+            if constexpr (ScanFastOp<T, OP>::enabled) {
+                uint32_t mx0 = 0u, mx1 = 0u;
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    mx0 = max(mx0, max(r.q[i].x + r.q[i].x - 1u, r.q[i].y + r.q[i].y - 1u));
+                    mx1 = max(mx1, max(r.q[i].z + r.q[i].z - 1u, r.q[i].w + r.q[i].w - 1u));
+                }
+                fast = __all_sync(0xffffffffu, max(mx0, mx1) <= 0xff000000u);
+            }
             // per row j: lane-serial fold of the lane's chunk, inclusive warp scan
             T rex[VR];   // exclusive prefix of this lane within row j (lane > 0)
             T rtot[VR];  // row totals
+            T run;
+            auto row_scans = [&](auto opv) {
+                using O = decltype(opv);
 #pragma unroll
-            for (int j = 0; j < VR; ++j) {
-                T v = r.e[j * RPER];
+                for (int j = 0; j < VR; ++j) {
+                    T v = r.e[j * RPER];
+                    if constexpr (O::three) {
+                        // two elements per FMNMX3
 #pragma unroll
-                for (int e = 1; e < RPER; ++e) v = OP::apply(v, r.e[j * RPER + e]);
-                if (LS_LAB_SKIP_ROWSCAN) {
-                    rex[j] = v;
-                    rtot[j] = v;
-                    continue;
+                        for (int e = 1; e + 1 < RPER; e += 2) v = O::apply3(v, r.e[j * RPER + e], r.e[j * RPER + e + 1]);
+                        if constexpr (RPER % 2 == 0) v = O::apply(v, r.e[j * RPER + RPER - 1]);
+                    } else {
+#pragma unroll
+                        for (int e = 1; e < RPER; ++e) v = O::apply(v, r.e[j * RPER + e]);
+                    }
+                    if (LS_LAB_SKIP_ROWSCAN) {
+                        rex[j] = v;
+                        rtot[j] = v;
+                        continue;
+                    }
+                    const T inc = warp_inclusive_scan<T, O>(v, lane);
+                    if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code) {
+                        // integer add: the exclusive prefix is inclusive - own value,
+                        // exact modulo 2^width, one shuffle fewer per row (+1-2 % i64)
+                        rex[j] = OP::apply(inc, (T)(0 - (typename std::make_unsigned<T>::type)v));
+                    } else {
+                        rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
+                    }
+                    rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
                 }
-                const T inc = warp_inclusive_scan<T, OP>(v, lane);
-                if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code) {
-                    // integer add: the exclusive prefix is inclusive - own value,
-                    // exact modulo 2^width, one shuffle fewer per row (+1-2 % i64)
-                    rex[j] = OP::apply(inc, (T)(0 - (typename std::make_unsigned<T>::type)v));
-                } else {
-                    rex[j] = __shfl_up_sync(0xffffffffu, inc, 1);
-                }
-                rtot[j] = __shfl_sync(0xffffffffu, inc, 31);
+                // serial row carry (Alg. 2): the warp's total over its rows
+                run = rtot[0];
+#pragma unroll
+                for (int j = 1; j < VR; ++j) run = O::apply(run, rtot[j]);
+            };
+            if constexpr (ScanFastOp<T, OP>::enabled) {
+                if (fast) row_scans(typename ScanFastOp<T, OP>::type{});
+                else row_scans(OP{});
+            } else {
+                row_scans(OP{});
             }
-            // serial row carry (Alg. 2): the warp's total over its rows
-            T run = rtot[0];
-#pragma unroll
-            for (int j = 1; j < VR; ++j) run = OP::apply(run, rtot[j]);
             if (lane == 0) warp_tot[warp] = run;
             named_bar_sync(1, SCAN_THREADS);  // (A) stage fully read; warp totals visible
             long long tm2 = LS_LAB_TIMING ? clock64() : 0;
@@ -674,46 +745,64 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int64_t valid = p.n - t * (int64_t)TILE_ELEMS;
             // rows before j, folded as the rows are stored (the same left fold as
             // the warp total above; no per-row array kept across the wait)
-            T rowpre = rtot[0];
+            auto fold_store = [&](auto opv, bool nan_fill) {
+                using O = decltype(opv);
+                T rowpre = rtot[0];
 #pragma unroll
-            for (int j = 0; j < VR; ++j) {
-                bool has = has0;
-                T acc = wcarry;
-                if (j > 0) {
-                    acc = has ? OP::apply(acc, rowpre) : rowpre;
-                    has = true;
-                    if (j + 1 < VR) rowpre = OP::apply(rowpre, rtot[j]);
-                }
-                if (lane > 0) { acc = has ? OP::apply(acc, rex[j]) : rex[j]; has = true; }
+                for (int j = 0; j < VR; ++j) {
+                    if (nan_fill) {
+                        // a NaN carry (fast chunks only): numpy keeps the left
+                        // NaN, so every result of the chunk is the carry
 #pragma unroll
-                for (int e = 0; e < RPER; ++e) {
-                    const T v = r.e[j * RPER + e];
-                    const bool first = (e == 0 && !has);
-                    if (EXCL) {
-                        r.e[j * RPER + e] = first ? ident : acc;
-                        acc = first ? v : OP::apply(acc, v);
+                        for (int e = 0; e < RPER; ++e) r.e[j * RPER + e] = wcarry;
                     } else {
-                        acc = first ? v : OP::apply(acc, v);
-                        r.e[j * RPER + e] = acc;
+                        bool has = has0;
+                        T acc = wcarry;
+                        if (j > 0) {
+                            acc = has ? O::apply(acc, rowpre) : rowpre;
+                            has = true;
+                            if (j + 1 < VR) rowpre = O::apply(rowpre, rtot[j]);
+                        }
+                        if (lane > 0) { acc = has ? O::apply(acc, rex[j]) : rex[j]; has = true; }
+#pragma unroll
+                        for (int e = 0; e < RPER; ++e) {
+                            const T v = r.e[j * RPER + e];
+                            const bool first = (e == 0 && !has);
+                            if (EXCL) {
+                                r.e[j * RPER + e] = first ? ident : acc;
+                                acc = first ? v : O::apply(acc, v);
+                            } else {
+                                acc = first ? v : O::apply(acc, v);
+                                r.e[j * RPER + e] = acc;
+                            }
+                        }
                     }
-                }
-                // 16-byte vector index of the lane's chunk in this row
-                const int64_t vec = (int64_t)warp * (WARP_BYTES / 16) + (int64_t)(j * 32 + lane) * VW;
-                if (VW == 2 && y256 && (!partial || (vec + 2) * PER <= valid)) {
-                    stg256(reinterpret_cast<uint8_t *>(yt) + vec * 16, r.q[j * VW], r.q[j * VW + 1]);
-                } else {
+                    // 16-byte vector index of the lane's chunk in this row
+                    const int64_t vec = (int64_t)warp * (WARP_BYTES / 16) + (int64_t)(j * 32 + lane) * VW;
+                    if (VW == 2 && y256 && (!partial || (vec + 2) * PER <= valid)) {
+                        stg256(reinterpret_cast<uint8_t *>(yt) + vec * 16, r.q[j * VW], r.q[j * VW + 1]);
+                    } else {
 #pragma unroll
-                    for (int u = 0; u < VW; ++u) {
-                        const int64_t vu = vec + u;
-                        if (!partial || (vu + 1) * PER <= valid) {
-                            stg128(reinterpret_cast<uint8_t *>(yt) + vu * 16, r.q[j * VW + u]);
-                        } else if (vu * PER < valid) {
+                        for (int u = 0; u < VW; ++u) {
+                            const int64_t vu = vec + u;
+                            if (!partial || (vu + 1) * PER <= valid) {
+                                stg128(reinterpret_cast<uint8_t *>(yt) + vu * 16, r.q[j * VW + u]);
+                            } else if (vu * PER < valid) {
 #pragma unroll
-                            for (int e = 0; e < PER; ++e)
-                                if (vu * PER + e < valid) yt[vu * PER + e] = r.e[(j * VW + u) * PER + e];
+                                for (int e = 0; e < PER; ++e)
+                                    if (vu * PER + e < valid) yt[vu * PER + e] = r.e[(j * VW + u) * PER + e];
+                            }
                         }
                     }
                 }
+            };
+            if constexpr (ScanFastOp<T, OP>::enabled) {
+                // the carry may be a zero or a NaN from outside the chunk: a zero
+                // never ties with the chunk's (nonzero) values; a NaN fills it
+                if (fast) fold_store(typename ScanFastOp<T, OP>::type{}, has0 && wcarry != wcarry);
+                else fold_store(OP{}, false);
+            } else {
+                fold_store(OP{}, false);
             }
             if (LS_LAB_TIMING && tid == 0) {
                 const long long tm4 = clock64();
