@@ -31,8 +31,10 @@ int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t 
     const bool wide = g_lab_dtype == 1 || g_lab_dtype == 3;
     void (*f)(const ScanParams) =
         g_lab_op == 1 ? pick<OpMax, SW, TILE, STAGES, VW>() : pick<OpAdd, SW, TILE, STAGES, VW>();
-    const size_t smem = scan_ws2_smem_bytes<int64_t, SW, TILE, STAGES>();
-    const int threads = ws2_threads<SW, false>();
+    // the 64-bit max kernel has a second reducer warp (ws2_red2)
+    const bool red2 = wide && g_lab_op == 1;
+    const size_t smem = scan_ws2_smem_bytes<int64_t, SW, TILE, STAGES, false, true>();
+    const int threads = red2 ? ws2_threads_x<SW, false, true>() : ws2_threads<SW, false>();
     if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int occ = 0, dev = 0, sms = 0;

@@ -20,8 +20,10 @@ constexpr int ws2_vw() {
 template <typename T, typename OP, bool EXCL>
 Launch fast_launch() {
     using C = FastCfg<sizeof(T)>;
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, false, ws2_vw<T, OP>()>, ws2_threads<C::kScanWarps, false>(),
-            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(), C::kTileBytes, C::kStages};
+    constexpr bool R2 = ws2_red2<T, OP, false, false>();
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, false, ws2_vw<T, OP>()>,
+            ws2_threads_x<C::kScanWarps, false, R2>(),
+            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, false, R2>(), C::kTileBytes, C::kStages};
 }
 
 template <typename T, typename OP, bool EXCL>

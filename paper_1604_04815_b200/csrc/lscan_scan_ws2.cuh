@@ -297,6 +297,17 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
 template <int SCAN_WARPS, bool MULTI>
 __host__ __device__ constexpr int ws2_threads() { return (SCAN_WARPS + (MULTI ? 5 : 3)) * 32; }
 
+// 64-bit max / min: the exact operator is four or five instructions and one
+// reducer warp publishes tile aggregates too late for the look-back (lab:
+// i64 max 340 -> 415 Gelem/s with the reducer pass skipped).  A second
+// reducer warp takes the upper half of each tile.
+template <typename T, typename OP, bool MULTI, bool SHIFT>
+__host__ __device__ constexpr bool ws2_red2() {
+    return !MULTI && !SHIFT && sizeof(T) == 8 && OP::idempotent;
+}
+template <int SCAN_WARPS, bool MULTI, bool RED2>
+__host__ __device__ constexpr int ws2_threads_x() { return ws2_threads<SCAN_WARPS, MULTI>() + (RED2 ? 32 : 0); }
+
 // Cross-GPU round chain helpers (MULTI): the exchange slot of (round k, gpu g)
 // in a GPU's exchange region, double-buffered by call parity so a fast GPU's
 // next call can never overwrite a slot a slow GPU still reads.
@@ -310,7 +321,9 @@ __device__ __forceinline__ uint64_t *xchg_slots(uint8_t *region, uint32_t xtag, 
 // one 256-bit store each, half the warp scans per element)
 template <typename T, typename OP, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool EXCL, bool MULTI = false,
           bool SHIFT = false, int VW = 1>
-__global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_kernel(const ScanParams p) {
+__global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, OP, MULTI, SHIFT>()>(), 1)
+    scan_ws2_kernel(const ScanParams p) {
+    constexpr bool RED2 = ws2_red2<T, OP, MULTI, SHIFT>();
     constexpr int SCAN_THREADS = SCAN_WARPS * 32;
     constexpr int V = TILE_BYTES / SCAN_THREADS / 16;  // rows (16-byte vectors) per lane
     constexpr int PER = 16 / (int)sizeof(T);           // elements per vector
@@ -321,6 +334,7 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     constexpr uint32_t ROW_BYTES = 512u * VW;
     static_assert(V % VW == 0 && (VW == 1 || VW == 2), "rows of one or two vectors per lane");
     constexpr int W_PROD = SCAN_WARPS, W_RED = SCAN_WARPS + 1, W_AUX = SCAN_WARPS + 2;
+    constexpr int W_RED2 = SCAN_WARPS + 3;  // RED2 only (never with MULTI)
     constexpr int W_PUSH = SCAN_WARPS + 3, W_GCHAIN = SCAN_WARPS + 4;  // MULTI only, CTA G-1 only
     static_assert(V >= 1 && TILE_BYTES % (SCAN_THREADS * 16) == 0, "whole rows per lane");
     static_assert(!(SHIFT && MULTI), "the shifted window is a single-GPU variant");
@@ -342,6 +356,8 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     int *pre_has = reinterpret_cast<int *>(pre + STAGES);
     T *warp_tot = reinterpret_cast<T *>(pre_has + STAGES + (STAGES & 1));
     T *warp_exc = warp_tot + SCAN_WARPS;
+    uint64_t *red2_ready = reinterpret_cast<uint64_t *>(warp_exc + SCAN_WARPS);  // RED2: upper half reduced
+    T *red2_val = reinterpret_cast<T *>(red2_ready + STAGES);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
@@ -360,7 +376,8 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
 #pragma unroll
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 2);
+            mbar_init(&empty[s], RED2 ? 3 : 2);
+            if (RED2) mbar_init(&red2_ready[s], 1);
             mbar_init(&pre_ready[s], 1);
             mbar_init(&pre_free[s], 1);
         }
@@ -469,6 +486,22 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             if (LS_LAB_TIMING) lab_t[4] += clock64() - tw;  // producer waiting for a free stage
             load_tile(k + STAGES);
         }
+    } else if (RED2 && warp == W_RED2) {
+        // ------------------------------------------ second reducer (RED2)
+        // the upper half of each tile; handed to the reducer through smem
+        for (int64_t k = 0; k < my_tiles; ++k) {
+            const int s = (int)(k % STAGES);
+            mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+            const T a = LS_LAB_SKIP_REDUCE ? ident
+                                           : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES + TILE_BYTES / 2,
+                                                                                 lane);
+            __syncwarp();
+            if (lane == 0) {
+                red2_val[s] = a;
+                mbar_arrive(&red2_ready[s]);
+                mbar_arrive(&empty[s]);
+            }
+        }
     } else if (warp == W_RED) {
         // ------------------------------------------------------------- reducer
         for (int64_t k = 0; k < my_tiles; ++k) {
@@ -476,10 +509,18 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
             const int64_t t = c + k * G;
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
             if (p.delay_red_ns > 0 && t % 3 == 1) debug_sleep(p.delay_red_ns);
-            const T a = LS_LAB_SKIP_REDUCE ? ident
-                        : SHIFT ? reduce_stage_shifted<T, OP, TILE_BYTES>(stages + s * STAGE_BYTES, lane,
-                                                                          p.x_shift / (int)sizeof(T))
-                                : reduce_stage<T, OP, TILE_BYTES>(stages + s * STAGE_BYTES, lane);
+            T a;
+            if constexpr (RED2) {
+                // lower half here, upper half from the second reducer, in order
+                a = LS_LAB_SKIP_REDUCE ? ident : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES, lane);
+                mbar_wait(&red2_ready[s], (uint32_t)((k / STAGES) & 1));
+                a = OP::apply(a, red2_val[s]);
+            } else {
+                a = LS_LAB_SKIP_REDUCE ? ident
+                    : SHIFT ? reduce_stage_shifted<T, OP, TILE_BYTES>(stages + s * STAGE_BYTES, lane,
+                                                                      p.x_shift / (int)sizeof(T))
+                            : reduce_stage<T, OP, TILE_BYTES>(stages + s * STAGE_BYTES, lane);
+            }
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&empty[s]);
@@ -859,10 +900,10 @@ __global__ void __launch_bounds__(ws2_threads<SCAN_WARPS, MULTI>(), 1) scan_ws2_
     }
 }
 
-template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool SHIFT = false>
+template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool SHIFT = false, bool RED2 = false>
 constexpr size_t scan_ws2_smem_bytes() {
     return (size_t)STAGES * (TILE_BYTES + (SHIFT ? 16 : 0)) + 4 * STAGES * 8 + STAGES * sizeof(T) +
-           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32;
+           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32 + (RED2 ? STAGES * (8 + sizeof(T)) : 0);
 }
 
 }  // namespace lscan
