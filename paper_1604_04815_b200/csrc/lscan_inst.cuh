@@ -29,9 +29,10 @@ Launch fast_launch() {
 template <typename T, typename OP, bool EXCL>
 Launch shift_launch() {
     using C = FastCfg<sizeof(T)>;
+    constexpr bool R2 = ws2_red2<T, OP, false, true>();
     return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true, ws2_vw<T, OP>()>,
-            ws2_threads<C::kScanWarps, false>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true>(),
-            C::kTileBytes, C::kStages};
+            ws2_threads_x<C::kScanWarps, false, R2>(),
+            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true, R2>(), C::kTileBytes, C::kStages};
 }
 
 template <typename T, typename OP, bool EXCL>
