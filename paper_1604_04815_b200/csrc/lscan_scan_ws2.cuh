@@ -126,35 +126,6 @@ __device__ __forceinline__ T reduce_stage_nan(const uint8_t *st, int lane, int l
     return x;
 }
 
-// exact reduction of window elements [lo, hi) of NVEC lane-strided 16-byte
-// vectors (the two halves of a shifted window, RED2)
-template <typename T, typename OP, int NVEC>
-__device__ __forceinline__ T reduce_window(const uint8_t *st, int lane, int lo, int hi) {
-    constexpr int PER = 16 / (int)sizeof(T);
-    const T ident = OP::template identity<T>();
-    T acc[4] = {ident, ident, ident, ident};
-    const uint32_t base = smem_u32(st);
-    constexpr int ITERS = (NVEC + 31) / 32;
-#pragma unroll 2
-    for (int i = 0; i < ITERS; i += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int v = (i + u) * 32 + lane;
-            if (v < NVEC) {
-                Regs<T, 1> r;
-                r.q[0] = lds128(base + (uint32_t)v * 16u);
-#pragma unroll
-                for (int e = 0; e < PER; ++e)
-                    if (v * PER + e >= lo && v * PER + e < hi) acc[u] = OP::apply(acc[u], r.e[e]);
-            }
-        }
-    }
-    const T x = warp_reduce_fixed<T, OP>(OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3])));
-    if constexpr (order_sensitive<T, OP>())
-        if (tie_class(x)) return tile_ties<T, OP>(st, lane, x, NVEC, lo, hi);
-    return x;
-}
-
 template <typename T, typename OP, int TILE_BYTES>
 __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
     constexpr int NV = TILE_BYTES / 16 / 32;  // 16-byte vectors per lane
@@ -519,18 +490,9 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
         for (int64_t k = 0; k < my_tiles; ++k) {
             const int s = (int)(k % STAGES);
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
-            T a;
-            if constexpr (SHIFT) {
-                // window vectors [NH, TILE/16 + 1): elements up to sh + TILE_ELEMS
-                constexpr int NH = TILE_BYTES / 32;
-                const int sh = p.x_shift / (int)sizeof(T);
-                a = reduce_window<T, OP, TILE_BYTES / 16 + 1 - NH>(stages + s * STAGE_BYTES + NH * 16, lane, 0,
-                                                                   sh + TILE_ELEMS - NH * PER);
-            } else {
-                a = LS_LAB_SKIP_REDUCE ? ident
-                                       : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES + TILE_BYTES / 2,
-                                                                             lane);
-            }
+            const T a = LS_LAB_SKIP_REDUCE ? ident
+                                           : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES + TILE_BYTES / 2,
+                                                                                 lane);
             __syncwarp();
             if (lane == 0) {
                 red2_val[s] = a;
@@ -548,13 +510,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             T a;
             if constexpr (RED2) {
                 // lower half here, upper half from the second reducer, in order
-                if constexpr (SHIFT) {
-                    constexpr int NH = TILE_BYTES / 32;
-                    a = reduce_window<T, OP, NH>(stages + s * STAGE_BYTES, lane, p.x_shift / (int)sizeof(T), NH * PER);
-                } else {
-                    a = LS_LAB_SKIP_REDUCE ? ident
-                                           : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES, lane);
-                }
+                a = LS_LAB_SKIP_REDUCE ? ident : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES, lane);
                 mbar_wait(&red2_ready[s], (uint32_t)((k / STAGES) & 1));
                 a = OP::apply(a, red2_val[s]);
             } else {
