@@ -16,6 +16,7 @@ ap.add_argument("--dtype", default="i32")
 ap.add_argument("--n", type=int, default=1 << 28)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--exclusive", action="store_true")
+ap.add_argument("--op", default="add", choices=["add", "max", "min"])
 a = ap.parse_args()
 dt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[a.dtype]
 if dt.is_floating_point:
@@ -25,6 +26,6 @@ else:
 y = torch.empty_like(x)
 fn = S.exclusive_scan if a.exclusive else S.inclusive_scan
 for _ in range(a.reps):
-    fn(x, out=y)
+    fn(x, out=y, op=a.op)
 torch.cuda.synchronize()
-print("done", a.dtype, a.n)
+print("done", a.dtype, a.op, a.n)
