@@ -88,6 +88,18 @@ ls_status ls_exclusive_sum(ls_dtype dt, const void *x, void *y, int64_t n,
                            const void *carry_in, void *total_out,
                            void *ws, size_t ws_bytes, void *stream);
 
+/* The strict left fold: y[j] = y[j-1] (+) x[j] one element after another,
+ * the reference's B = 1 path (ChainConfig(b=1), chained.py:290-313), which
+ * is bit-identical to sequential_scan (reference.py:61-67) for every
+ * operator — float add included, where the parallel scans above associate
+ * differently and match only within the envelope.  One CTA runs the
+ * dependent chain (about one add latency per element; x streamed in by TMA,
+ * y stored by separate warps), so it is an exactness mode, not a fast path.
+ * Same conventions as ls_inclusive_scan (any alignment, x == y allowed,
+ * carry_in / total_out); exclusive != 0 gives the exclusive form. */
+ls_status ls_ordered_scan(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
+                          const void *carry_in, void *total_out, void *stream);
+
 /* total_out = x[0] (+) ... (+) x[n-1] (device scalar; identity for n == 0),
  * deterministic for a given device; the per-shard total of the multi-GPU
  * carry exchange. */
@@ -146,6 +158,13 @@ ls_status ls_ipc_close(void *dev_ptr);
  * chunks.  Blocks until y is complete.  device < 0 = current device. */
 ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
                        int exclusive, int device);
+/* ls_scan_host with flags: LS_HOST_EXCLUSIVE, LS_HOST_ORDERED (every chunk
+ * through ls_ordered_scan, the carry chained between chunks: the whole array
+ * is one strict left fold — ChainConfig(b=1)). */
+#define LS_HOST_EXCLUSIVE 1
+#define LS_HOST_ORDERED 2
+ls_status ls_scan_host_ex(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
+                          int flags, int device);
 ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n,
                                 int exclusive, int device);
 

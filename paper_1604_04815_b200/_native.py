@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(LIB_DIR, "liblscan.so")
 
 SOURCES = ["lscan_api.cu", "lscan_host.cu", "lscan_inst_i32.cu", "lscan_inst_i64.cu",
            "lscan_inst_f32.cu", "lscan_inst_f64.cu"]
-HEADERS = ["lscan_common.cuh", "lscan_ptx.cuh", "lscan_cluster.cuh", "lscan_generic.cuh", "lscan_scan_ws2.cuh", "lscan_dispatch.h",
+HEADERS = ["lscan_common.cuh", "lscan_ptx.cuh", "lscan_cluster.cuh", "lscan_generic.cuh", "lscan_scan_ws2.cuh", "lscan_ordered.cuh", "lscan_dispatch.h",
            "lscan_inst.cuh"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -40,6 +40,9 @@ LS_I32, LS_I64, LS_F32, LS_F64 = 0, 1, 2, 3
 
 # ls_op
 LS_OP_ADD, LS_OP_MAX, LS_OP_MIN = 0, 1, 2
+
+# ls_scan_host_ex flags
+LS_HOST_EXCLUSIVE, LS_HOST_ORDERED = 1, 2
 OPS = {"add": LS_OP_ADD, "max": LS_OP_MAX, "min": LS_OP_MIN}
 
 EXPORTED = [
@@ -49,7 +52,7 @@ EXPORTED = [
     "ls_workspace_error", "ls_status_string", "ls_last_error_detail", "ls_abi_version",
     "ls_query_config", "ls_launch_count", "ls_xchg_bytes", "ls_inclusive_scan_multi", "ls_exclusive_scan_multi",
     "ls_device_alloc", "ls_device_free", "ls_ipc_get_handle", "ls_ipc_open", "ls_ipc_close", "ls_debug_slot_stress",
-    "ls_debug_force_path", "ls_query_cluster", "ls_query_multi_config",
+    "ls_debug_force_path", "ls_query_cluster", "ls_query_multi_config", "ls_ordered_scan", "ls_scan_host_ex",
 ]
 
 
@@ -123,6 +126,8 @@ def lib():
             "ls_reduce_sum": (ci, [ci, vp, i64, vp, vp, sz, vp]),
             "ls_carry_from_totals": (ci, [ci, ci, vp, i64, i64, vp, vp]),
             "ls_scan_host": (ci, [ci, ci, vp, vp, i64, ci, ci]),
+            "ls_scan_host_ex": (ci, [ci, ci, vp, vp, i64, ci, ci]),
+            "ls_ordered_scan": (ci, [ci, ci, vp, vp, i64, ci, vp, vp, vp]),
             "ls_inclusive_sum_host": (ci, [ci, vp, vp, i64, ci, ci]),
             "ls_debug_config": (ci, [i64, i64, ci]),
             "ls_debug_perturb": (ci, [i64, i64, i64]),

@@ -17,11 +17,18 @@ The scan runs on the device through the C ABI (``ls_inclusive_sum_host``):
 the host array is streamed through the GPU in chunks with copy-in, scan and
 copy-out overlapped.  There is no CPU path.
 
-``ChainConfig`` keeps the reference's fields (chained.py:205-234).  On the
-GPU, ``b`` (workers) and ``geometry`` (block shape) are decided by the
-device (persistent CTAs = co-resident capacity, compile-time tiles) and are
-accepted for compatibility — so float add always follows the reference's
-B > 1 contract (the envelope), never the B == 1 bit-exact fold.
+``ChainConfig`` keeps the reference's fields (chained.py:205-234) and the
+drop-in accepts the reference's own ``ChainConfig`` objects.  On the GPU the
+worker count and block shape of the parallel scan are decided by the device
+(persistent CTAs = co-resident capacity, compile-time tiles), so ``geometry``
+and any ``b > 1`` select the same kernel: float add then follows the
+reference's B > 1 contract (within the envelope, bench.py:90-114), integers
+and max/min are bit-exact regardless.  ``b == 1`` keeps the reference's B = 1
+contract — bit-identical to the sequential fold, float add included
+(chained.py:290-313; test_acceptance.py:85-111): float add with ``b == 1``
+runs the strict left fold on the device (``ls_ordered_scan``: one CTA, one
+dependent add per element, ~0.3-0.5 Gelem/s), every other case is already
+bit-exact on the parallel kernel.
 ``spin_budget`` and ``corrupt_slot`` map onto the device watchdog and fault
 injection and raise the reference's ``LivenessError``.  ``protocol_checks``
 needs no per-call check: every device slot is written once per call by
@@ -39,6 +46,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
+from ._compat import compat
 from . import _native as N
 from .errors import LivenessError, ProtocolViolation, raise_for_status  # noqa: F401
 from .operators import DTYPES, require_device_operator
@@ -114,16 +122,16 @@ def _scan_host(problem, config: Optional[ChainConfig], exclusive: bool) -> np.nd
     dtype = require_device_operator(op)
     x = problem.x
     if x.ndim != 1:
-        raise ShapeError(f"input must be 1-D, got shape {x.shape}")
+        raise compat(ShapeError)(f"input must be 1-D, got shape {x.shape}")
     if x.dtype != dtype:
         # the reference silently computes in x's dtype; the drop-in refuses
         # the mismatch instead of guessing
-        raise ShapeError(f"input dtype {x.dtype} does not match operator dtype {dtype}")
+        raise compat(ShapeError)(f"input dtype {x.dtype} does not match operator dtype {dtype}")
     out = problem.out if problem.out is not None else np.empty_like(x)
     if out.shape != x.shape or out.dtype != dtype:
-        raise ShapeError("out must match the input's shape and dtype")
+        raise compat(ShapeError)("out must match the input's shape and dtype")
     if not out.flags.c_contiguous or not out.flags.writeable:
-        raise ShapeError("out must be a writeable C-contiguous array")
+        raise compat(ShapeError)("out must be a writeable C-contiguous array")
     n = x.size
     if n == 0:
         return out
@@ -137,9 +145,11 @@ def _scan_host(problem, config: Optional[ChainConfig], exclusive: bool) -> np.nd
     # both arrays are contiguous, so overlapping bounds mean real overlap
     aliased = problem.out is not None and np.may_share_memory(out, x)
     if aliased and out.ctypes.data != x.ctypes.data:
-        raise ShapeError("out overlaps x without being the same array (only exact in-place is supported)")
-    rc = N.lib().ls_scan_host(N.OPS[op.name], NP_DT[dtype], x.ctypes.data, out.ctypes.data, n,
-                              1 if exclusive else 0, -1)
+        raise compat(ShapeError)("out overlaps x without being the same array (only exact in-place is supported)")
+    flags = N.LS_HOST_EXCLUSIVE if exclusive else 0
+    if config is not None and config.b == 1 and op.name == "add" and dtype.kind == "f":
+        flags |= N.LS_HOST_ORDERED  # the B = 1 bit-exact fold (chained.py:290-313)
+    rc = N.lib().ls_scan_host_ex(N.OPS[op.name], NP_DT[dtype], x.ctypes.data, out.ctypes.data, n, flags, -1)
     raise_for_status(rc)
     return out
 

@@ -206,6 +206,10 @@ ls_status device_state(DevState **out) {
                             "occupancy query");
                     d.occ_shift[dt][op][ex] = occs;
                 }
+                for (int ex = 0; ex < 2; ++ex)
+                    LS_CUDA(cudaFuncSetAttribute((const void *)k.ordered[op][ex].fn,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.ordered[op][ex].smem),
+                            "cudaFuncSetAttribute(max dynamic smem)");
                 int occ = 0;
                 LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.reduce_fn[op], kReduceThreads, 0),
                         "occupancy");
@@ -579,6 +583,37 @@ ls_status ls_exclusive_sum(ls_dtype dt, const void *x, void *y, int64_t n, const
     return scan_impl(LS_OP_ADD, dt, x, y, n, carry_in, total_out, ws, ws_bytes, stream, true);
 }
 
+ls_status ls_ordered_scan(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
+                          const void *carry_in, void *total_out, void *stream) {
+    if (!valid_dtype(dt)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported dtype code %d", (int)dt);
+    if (!valid_op(op)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported operator code %d", (int)op);
+    const int es = elem_size(dt);
+    if (n < 0) return fail(LS_ERR_INVALID_ARG, "n must be >= 0, got %lld", (long long)n);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n > 0 && (!x || !y)) return fail(LS_ERR_INVALID_ARG, "x and y must be non-NULL for n > 0");
+    if (((uintptr_t)x % es) || ((uintptr_t)y % es))
+        return fail(LS_ERR_INVALID_ARG, "x and y must be aligned to the element size (%d)", es);
+    if (x != y && n > 0 && ranges_overlap(x, y, (size_t)n * es))
+        return fail(LS_ERR_INVALID_ARG, "x and y overlap without being identical (only exact in-place is allowed)");
+    if (total_out && carry_in && total_out == carry_in)
+        return fail(LS_ERR_INVALID_ARG, "total_out must not alias carry_in");
+    if (n == 0) return total_out ? identity_fill(op, dt, total_out, carry_in, s) : LS_OK;
+    DevState *d = nullptr;
+    ls_status st = device_state(&d);
+    if (st != LS_OK) return st;
+    const Launch &L = K(dt).ordered[op][exclusive ? 1 : 0];
+    ScanParams p{};
+    p.x = x;
+    p.y = y;
+    p.n = n;
+    p.carry_in = carry_in;
+    p.total_out = total_out;
+    L.fn<<<1, L.threads, L.smem, s>>>(p);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    LS_CUDA(cudaGetLastError(), "ordered scan kernel launch");
+    return LS_OK;
+}
+
 ls_status ls_reduce(ls_op op, ls_dtype dt, const void *x, int64_t n, void *total_out, void *ws, size_t ws_bytes,
                     void *stream) {
     if (!valid_dtype(dt)) return fail(LS_ERR_UNSUPPORTED_DTYPE, "unsupported dtype code %d", (int)dt);
@@ -680,7 +715,10 @@ static ls_status scan_multi_impl(ls_op op, ls_dtype dt, const void *x, void *y, 
     p.world = world;
     p.xchg = static_cast<uint8_t *>(xchg);
     p.xchg_peers = reinterpret_cast<uint64_t *const *>(peers);
-    p.xchg_rounds = std::max<int64_t>(M, 1);
+    // the parity halves' stride is the region's fixed capacity (in rounds),
+    // never this call's round count: consecutive calls with different n (the
+    // short last chunk of scan_host) must keep their halves apart
+    p.xchg_rounds = (int64_t)((xchg_bytes - kXchgSlotBase) / (2 * (size_t)world * (es == 4 ? 8 : 16)));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);

@@ -51,6 +51,7 @@ struct DtypeKernels {
     int ws2_vw[kNumOps];         // the persistent kernel's scanner row width in vectors (y alignment 16 * vw)
     Launch shift[kNumOps][2];    // [op][exclusive]: x 16 bytes misaligned, y aligned (shifted TMA window)
     Launch cluster[kNumOps][2][kClusterGeoms];  // [op][exclusive][small, mid, large]: latency kernel (any alignment)
+    Launch ordered[kNumOps][2];  // [op][exclusive]: strict left fold, one CTA (the reference's B = 1 path)
     const void *reduce_fn[kNumOps];
     void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s);
     void (*launch_carry)(int op, const void *totals, int64_t rank, void *carry_out, cudaStream_t s);

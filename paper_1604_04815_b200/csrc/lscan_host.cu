@@ -147,28 +147,15 @@ void parallel_memcpy(void *dst, const void *src, size_t bytes) {
     for (auto &t : th) t.join();
 }
 
-}  // namespace
-
-extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
-                                  int device) {
-    if (dt < LS_I32 || dt > LS_F64 || op < LS_OP_ADD || op > LS_OP_MIN) return LS_ERR_UNSUPPORTED_DTYPE;
-    if (n < 0 || (n > 0 && (!x || !y))) return LS_ERR_INVALID_ARG;
-    if (n == 0) return LS_OK;
+// The chunk pipeline proper.  Returns at the first failure; the caller
+// (ls_scan_host_ex) synchronises the three streams and restores the device
+// on every path, so no copy is still writing into y or the staging buffers
+// when an error is reported.
+ls_status run_pipeline(HostCtx *c, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int flags) {
     const int es = esize(dt);
-    if (x != y) {
-        const uintptr_t a = (uintptr_t)x, b = (uintptr_t)y, bytes = (uintptr_t)n * es;
-        if (a < b + bytes && b < a + bytes) return LS_ERR_INVALID_ARG;
-    }
-    int dev = device;
-    if (dev < 0) HC(cudaGetDevice(&dev), "cudaGetDevice");
-    int prev = 0;
-    HC(cudaGetDevice(&prev), "cudaGetDevice");
-    if (prev != dev) HC(cudaSetDevice(dev), "cudaSetDevice");
-    HostCtx *c = nullptr;
-    ls_status st = ctx_for(dev, &c);
-    if (st != LS_OK) return st;
-    std::lock_guard<std::mutex> lk(c->mu);
-
+    const bool exclusive = (flags & LS_HOST_EXCLUSIVE) != 0;
+    const bool ordered = (flags & LS_HOST_ORDERED) != 0;
+    ls_status st = LS_OK;
     const bool direct = is_pinned(x) && is_pinned(y);
     if (!direct && (st = ensure_staging(c)) != LS_OK) return st;
 
@@ -207,8 +194,12 @@ extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y,
         HC(cudaStreamWaitEvent(c->s_comp, c->ev_in[b], 0), "wait copy-in");
         const void *cin = k ? carry + 16 * ((k - 1) & 1) : nullptr;
         void *cout = carry + 16 * (k & 1);
-        st = exclusive ? ls_exclusive_scan(op, dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp)
-                       : ls_inclusive_scan(op, dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp);
+        if (ordered)
+            st = ls_ordered_scan(op, dt, c->dbuf[b], c->dbuf[b], len, exclusive ? 1 : 0, cin, cout, c->s_comp);
+        else if (exclusive)
+            st = ls_exclusive_scan(op, dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp);
+        else
+            st = ls_inclusive_scan(op, dt, c->dbuf[b], c->dbuf[b], len, cin, cout, c->ws, c->ws_bytes, c->s_comp);
         if (st != LS_OK) return st;
         HC(cudaEventRecord(c->ev_comp[b], c->s_comp), "event");
         HC(cudaStreamWaitEvent(c->s_out, c->ev_comp[b], 0), "wait scan");
@@ -220,10 +211,51 @@ extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y,
         for (int64_t k = std::max<int64_t>(0, nchunks - kBufs); k < nchunks; ++k)
             if ((st = drain(k)) != LS_OK) return st;
     }
-    HC(cudaStreamSynchronize(c->s_out), "final sync");
-    HC(cudaStreamSynchronize(c->s_comp), "final sync");
-    if (prev != dev) HC(cudaSetDevice(prev), "cudaSetDevice");
     return LS_OK;
+}
+
+}  // namespace
+
+extern "C" ls_status ls_scan_host_ex(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int flags,
+                                     int device) {
+    if (dt < LS_I32 || dt > LS_F64 || op < LS_OP_ADD || op > LS_OP_MIN) return LS_ERR_UNSUPPORTED_DTYPE;
+    if (n < 0 || (n > 0 && (!x || !y)) || (flags & ~(LS_HOST_EXCLUSIVE | LS_HOST_ORDERED))) return LS_ERR_INVALID_ARG;
+    if (n == 0) return LS_OK;
+    const int es = esize(dt);
+    if (x != y) {
+        const uintptr_t a = (uintptr_t)x, b = (uintptr_t)y, bytes = (uintptr_t)n * es;
+        if (a < b + bytes && b < a + bytes) return LS_ERR_INVALID_ARG;
+    }
+    int prev = 0;
+    HC(cudaGetDevice(&prev), "cudaGetDevice");
+    int dev = device < 0 ? prev : device;
+    if (prev != dev) HC(cudaSetDevice(dev), "cudaSetDevice");
+    HostCtx *c = nullptr;
+    ls_status st = ctx_for(dev, &c);
+    if (st == LS_OK) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        st = run_pipeline(c, op, dt, x, y, n, flags);
+        // one exit for every outcome: nothing of this call is still in flight
+        // when it returns, error or not
+        const cudaError_t e_out = cudaStreamSynchronize(c->s_out);
+        const cudaError_t e_comp = cudaStreamSynchronize(c->s_comp);
+        const cudaError_t e_in = cudaStreamSynchronize(c->s_in);
+        if (st == LS_OK) {
+            if (e_out != cudaSuccess) st = host_fail(LS_ERR_CUDA, e_out, "final sync (copy-out)");
+            else if (e_comp != cudaSuccess) st = host_fail(LS_ERR_CUDA, e_comp, "final sync (scan)");
+            else if (e_in != cudaSuccess) st = host_fail(LS_ERR_CUDA, e_in, "final sync (copy-in)");
+        }
+    }
+    if (prev != dev) {
+        const cudaError_t e = cudaSetDevice(prev);
+        if (st == LS_OK && e != cudaSuccess) st = host_fail(LS_ERR_CUDA, e, "cudaSetDevice (restore)");
+    }
+    return st;
+}
+
+extern "C" ls_status ls_scan_host(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,
+                                  int device) {
+    return ls_scan_host_ex(op, dt, x, y, n, exclusive ? LS_HOST_EXCLUSIVE : 0, device);
 }
 
 extern "C" ls_status ls_inclusive_sum_host(ls_dtype dt, const void *x, void *y, int64_t n, int exclusive,

@@ -4,6 +4,7 @@
 #include "lscan_dispatch.h"
 #include "lscan_cluster.cuh"
 #include "lscan_generic.cuh"
+#include "lscan_ordered.cuh"
 #include "lscan_scan_ws2.cuh"
 
 namespace lscan {
@@ -38,9 +39,12 @@ Launch shift_launch() {
 template <typename T, typename OP, bool EXCL>
 Launch multi_launch() {
     using C = MultiCfg<sizeof(T)>;
-    // the fused multi-GPU kernel keeps 16-byte rows (measured 777 vs 765
-    // Gelem/s at world size 1 with 32-byte rows)
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true, false, 1>,
+    // the fused multi-GPU kernel keeps 16-byte rows for 32-bit types
+    // (measured 777 vs 765 Gelem/s at world size 1 with 32-byte rows); 64-bit
+    // types take 32-byte rows, which halve the per-row carries a lane keeps
+    // live (16-byte rows spilled 12 bytes in the i64 instantiations)
+    constexpr int VW = sizeof(T) == 8 ? 2 : 1;
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true, false, VW>,
             ws2_threads<C::kScanWarps, true>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(),
             C::kTileBytes, C::kStages};
 }
@@ -80,6 +84,8 @@ void fill_op(DtypeKernels &k) {
     k.shift[OP::code][0] = shift_launch<T, OP, false>();
     k.shift[OP::code][1] = shift_launch<T, OP, true>();
     k.reduce_fn[OP::code] = (const void *)&reduce_kernel<T, OP, kReduceThreads>;
+    k.ordered[OP::code][0] = {&scan_ordered_kernel<T, OP, false>, kOrdThreads, kOrdSmemBytes, kOrdStageBytes, kOrdStages};
+    k.ordered[OP::code][1] = {&scan_ordered_kernel<T, OP, true>, kOrdThreads, kOrdSmemBytes, kOrdStageBytes, kOrdStages};
 }
 
 template <typename T>

@@ -2,11 +2,20 @@
 
 chained.py:48-53 (LivenessError, ProtocolViolation), reference.py:34-35
 (ShapeError), operators.py:34-35 (UnsupportedOperatorError).
+
+Drop-in compatibility: a caller written against the reference catches the
+reference's own classes (``except chainscan.LivenessError``).  When the
+reference package is loaded in the process (``chainscan`` in
+``sys.modules`` — a caller that names its classes has imported it), every
+error the drop-in raises is an instance of BOTH this package's class and
+the reference class of the same name (``compat``), so either ``except``
+clause matches.  Nothing here imports the reference.
 """
 
 from __future__ import annotations
 
 from . import _native as N
+from ._compat import compat
 from .operators import UnsupportedOperatorError
 from .problem import ShapeError
 
@@ -34,13 +43,13 @@ def raise_for_status(code: int) -> None:
     name = N.status_string(code)
     msg = f"{name}: {detail}" if detail else name
     if code == N.LS_ERR_INVALID_ARG:
-        raise ShapeError(msg)
+        raise compat(ShapeError)(msg)
     if code == N.LS_ERR_UNSUPPORTED_DTYPE:
-        raise UnsupportedOperatorError(msg)
+        raise compat(UnsupportedOperatorError)(msg)
     if code == N.LS_ERR_LIVENESS:
-        raise LivenessError(msg)
+        raise compat(LivenessError)(msg)
     if code == N.LS_ERR_PROTOCOL:
-        raise ProtocolViolation(msg)
+        raise compat(ProtocolViolation)(msg)
     if code == N.LS_ERR_WORKSPACE:
         raise WorkspaceError(msg)
     raise DeviceError(msg)

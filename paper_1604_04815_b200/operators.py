@@ -17,6 +17,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._compat import compat
+
 # operators.py:24-29
 DTYPES = {
     "i32": np.dtype(np.int32),
@@ -38,11 +40,11 @@ def parse_dtype(token) -> np.dtype:
     if isinstance(token, np.dtype):
         if token in DTYPES.values():
             return token
-        raise UnsupportedOperatorError(f"unsupported element type {token}")
+        raise compat(UnsupportedOperatorError)(f"unsupported element type {token}")
     try:
         return DTYPES[token]
     except (KeyError, TypeError):
-        raise UnsupportedOperatorError(
+        raise compat(UnsupportedOperatorError)(
             f"unknown element type {token!r}; supported: {', '.join(DTYPES)}") from None
 
 
@@ -51,7 +53,7 @@ def dtype_token(dtype) -> str:
     for tok, dt in DTYPES.items():
         if dt == dtype:
             return tok
-    raise UnsupportedOperatorError(f"no token for dtype {dtype}")
+    raise compat(UnsupportedOperatorError)(f"no token for dtype {dtype}")
 
 
 @dataclass(frozen=True)
@@ -81,7 +83,7 @@ def make_operator(name: str, elem_type) -> ScanOperator:
     elif name == "min":
         identity = dtype.type(np.iinfo(dtype).max if dtype.kind == "i" else np.inf)
     else:
-        raise UnsupportedOperatorError(
+        raise compat(UnsupportedOperatorError)(
             f"unknown operator {name!r}; supported: {', '.join(OPERATOR_NAMES)}")
     return ScanOperator(name=name, dtype=dtype, identity=identity)
 
@@ -90,6 +92,6 @@ def require_device_operator(op) -> np.dtype:
     """The operator must be one the device implements (add / max / min)."""
     name = getattr(op, "name", None)
     if name not in DEVICE_OPERATORS:
-        raise UnsupportedOperatorError(
+        raise compat(UnsupportedOperatorError)(
             f"operator {name!r} has no device scan; supported: {', '.join(DEVICE_OPERATORS)}")
     return parse_dtype(np.dtype(op.dtype))

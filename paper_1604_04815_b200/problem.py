@@ -7,6 +7,8 @@ from typing import Optional
 
 import numpy as np
 
+from ._compat import compat
+
 
 class ShapeError(ValueError):
     """Raised when an input shape violates a precondition (reference.py:34-35)."""
@@ -27,9 +29,9 @@ class ScanProblem:
     def __post_init__(self):
         self.x = np.asanyarray(self.x)
         if self.x.ndim != 1:
-            raise ShapeError(f"input must be 1-D, got shape {self.x.shape}")
+            raise compat(ShapeError)(f"input must be 1-D, got shape {self.x.shape}")
         if self.out is not None and self.out.shape != self.x.shape:
-            raise ShapeError("out shape must match input shape")
+            raise compat(ShapeError)("out shape must match input shape")
 
     def resolve_out(self) -> np.ndarray:
         return self.out if self.out is not None else np.empty_like(self.x)

@@ -18,6 +18,7 @@ from typing import Dict, Optional, Tuple
 
 import torch
 
+from ._compat import compat
 from . import _native as N
 from .errors import raise_for_status
 from .operators import UnsupportedOperatorError
@@ -38,7 +39,7 @@ def dtype_code(dtype: torch.dtype) -> int:
     try:
         return TORCH_DT[dtype]
     except KeyError:
-        raise UnsupportedOperatorError(
+        raise compat(UnsupportedOperatorError)(
             f"unsupported element type {dtype}; supported: int32, int64, float32, float64") from None
 
 
@@ -65,7 +66,7 @@ def _check_1d(x: torch.Tensor, what: str = "input") -> None:
     if not isinstance(x, torch.Tensor):
         raise TypeError(f"{what} must be a torch.Tensor")
     if x.dim() != 1:
-        raise ShapeError(f"{what} must be 1-D, got shape {tuple(x.shape)}")
+        raise compat(ShapeError)(f"{what} must be 1-D, got shape {tuple(x.shape)}")
     if not x.is_cuda:
         raise ValueError(f"{what} must be a CUDA tensor (there is no CPU path)")
 
@@ -82,7 +83,7 @@ def op_code(op: str) -> int:
     try:
         return N.OPS[op]
     except KeyError:
-        raise UnsupportedOperatorError(f"unknown operator {op!r}; supported: {', '.join(N.OPS)}") from None
+        raise compat(UnsupportedOperatorError)(f"unknown operator {op!r}; supported: {', '.join(N.OPS)}") from None
 
 
 # the raw cudaStream_t of a device's current stream, without building a Stream
@@ -117,7 +118,7 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
     if type(x) is not torch.Tensor and not isinstance(x, torch.Tensor):
         raise TypeError("input must be a torch.Tensor")
     if x.dim() != 1:
-        raise ShapeError(f"input must be 1-D, got shape {tuple(x.shape)}")
+        raise compat(ShapeError)(f"input must be 1-D, got shape {tuple(x.shape)}")
     if not x.is_cuda:
         raise ValueError("input must be a CUDA tensor (there is no CPU path)")
     dt = TORCH_DT.get(x.dtype)
@@ -133,14 +134,14 @@ def _scan(x: torch.Tensor, out: Optional[torch.Tensor], carry_in, total_out, exc
     elif out is not x:
         _check_1d(out, "out")
         if out.numel() != n:
-            raise ShapeError("out shape must match input shape")
+            raise compat(ShapeError)("out shape must match input shape")
         if out.dtype != x.dtype or out.get_device() != idx:
             raise ValueError("out must have the input's dtype and device")
         if not out.is_contiguous():
-            raise ShapeError("out must be contiguous")
+            raise compat(ShapeError)("out must be contiguous")
     if not x.is_contiguous():
         if out is x:
-            raise ShapeError("in-place scan needs a contiguous tensor")
+            raise compat(ShapeError)("in-place scan needs a contiguous tensor")
         x = x.contiguous()
     prev = _get_device()
     switch = idx != prev
@@ -182,6 +183,38 @@ def exclusive_scan(x: torch.Tensor, out: Optional[torch.Tensor] = None, *,
                    total_out: Optional[torch.Tensor] = None, op: str = "add") -> torch.Tensor:
     """y[0] = carry (or the identity), y[j] = carry (+) x[0] (+) ... (+) x[j-1]."""
     return _scan(x, out, carry_in, total_out, exclusive=True, op=op)
+
+
+def ordered_scan(x: torch.Tensor, out: Optional[torch.Tensor] = None, *, exclusive: bool = False,
+                 carry_in: Optional[torch.Tensor] = None, total_out: Optional[torch.Tensor] = None,
+                 op: str = "add") -> torch.Tensor:
+    """The strict left fold on the device (``ls_ordered_scan``): y[j] =
+    y[j-1] (+) x[j] in sequence, bit-identical to the reference's
+    ``sequential_scan`` and to its ``ChainConfig(b=1)`` path (chained.py:290-313)
+    for every operator, float add included.  One CTA runs the dependent chain
+    (an exactness mode at roughly one add latency per element, not a fast
+    path); ``inclusive_scan`` is the parallel scan."""
+    _check_1d(x)
+    dt = dtype_code(x.dtype)
+    oc = op_code(op)
+    n = x.numel()
+    if out is None:
+        out = torch.empty_like(x, memory_format=torch.contiguous_format)
+    elif out is not x:
+        _check_1d(out, "out")
+        if out.numel() != n or out.dtype != x.dtype or out.device != x.device or not out.is_contiguous():
+            raise compat(ShapeError)("out must be a contiguous tensor of x's shape, dtype and device")
+    if not x.is_contiguous():
+        if out is x:
+            raise compat(ShapeError)("in-place scan needs a contiguous tensor")
+        x = x.contiguous()
+    stream = torch.cuda.current_stream(x.device)
+    with torch.cuda.device(x.device):
+        rc = N.lib().ls_ordered_scan(oc, dt, x.data_ptr() if n else None, out.data_ptr() if n else None, n,
+                                     1 if exclusive else 0, _scalar_ptr(carry_in, x, "carry_in"),
+                                     _scalar_ptr(total_out, x, "total_out"), stream.cuda_stream)
+    raise_for_status(rc)
+    return out
 
 
 def reduce(x: torch.Tensor, total_out: Optional[torch.Tensor] = None, op: str = "add") -> torch.Tensor:
