@@ -131,9 +131,11 @@ ls_status ls_carry_from_totals(ls_op op, ls_dtype dt, const void *totals, int64_
  *   region as mapped in this process (entry rank = xchg);
  * grid > 0 caps the CTAs (equal on every GPU), 0 = the device's capacity.
  * total_out receives the GLOBAL total.  All GPUs must make the same sequence
- * of calls.  The debug watchdog applies, but these calls never synchronise on
- * it (all GPUs of a call must be in flight together): read the outcome with
- * ls_workspace_error. */
+ * of calls.  A watchdog is always armed (a large default probe budget, or the
+ * ls_debug_config budget): a peer that died or never launches its half of a
+ * call turns into LS_ERR_LIVENESS in the workspace instead of a hang.  These
+ * calls never synchronise on it (all GPUs of a call must be in flight
+ * together): read the outcome with ls_workspace_error. */
 size_t ls_xchg_bytes(ls_dtype dt, int world, int64_t n_local);
 ls_status ls_inclusive_scan_multi(ls_op op, ls_dtype dt, const void *x, void *y, int64_t n_local,
                                   const void *carry_in, void *total_out, void *ws, size_t ws_bytes,

@@ -13,7 +13,13 @@ best of ``--runs``; ``--timing device`` times the kernel alone on a
 device-resident array with CUDA events.  ``--inject-slot-fault TILE`` makes
 that tile publish the identity (ChainConfig.corrupt_slot), so validation
 fails and the exit code is 1 — the reference's hidden flag (cli.py:79-80).
-Validation is on the device (records.device_check).
+Validation follows the reference's rule on the host after timing
+(records.host_check: the numpy sequential fold, raw-bit comparison for
+integers and max/min, the envelope for float add).  The reference's
+block-geometry flags (``--warp-width``, ``--k``, ``--warps-per-block``,
+``--block-scan-mode``) are accepted and validated like the reference's
+(WarpGeometry, warp.py:42-82); the device's tile shape is fixed at compile
+time, so they do not change the kernel.
 """
 
 from __future__ import annotations
@@ -32,22 +38,35 @@ from .chained import ChainConfig, chained_exclusive_scan, chained_scan
 from .errors import LivenessError, ProtocolViolation
 from .operators import DTYPES, OPERATOR_NAMES, make_operator
 from .problem import ScanProblem, ShapeError
-from .records import BenchRecord, write_records
+from .records import BenchRecord, host_check, write_records
 
 DEFAULT_NS = [2 ** 20, 2 ** 22, 2 ** 24, 2 ** 26]                                 # bench.py:47
 PAPER_NS = [32_000_000, 64_000_000, 128_000_000, 256_000_000, 512_000_000]        # bench.py:45
 ALGORITHMS = ("chained",)
+REFERENCE_ALGORITHMS = ("sequential", "hillis-steele", "blelloch", "matrix", "chained")  # bench.py:36
+WORKERS_ENV = "CHAINSCAN_WORKERS"  # cli.py:36
 
 
 def build_parser() -> argparse.ArgumentParser:
-    p = argparse.ArgumentParser(prog="lscan", description="B200 single-pass scan benchmarks (chainscan-compatible).")
+    p = argparse.ArgumentParser(
+        prog="lscan",
+        description="B200 single-pass scan benchmarks (chainscan-compatible). The reference's CPU algorithms "
+                    "and its `simulate` subcommand (the scheduler model) are not provided.")
     p.add_argument("--version", action="version", version=f"lscan {__version__}")
-    p.add_argument("--algo", default="chained", help="scan algorithm (only 'chained' runs on the device)")
+    p.add_argument("--algo", choices=REFERENCE_ALGORITHMS, default="chained",
+                   help="scan algorithm (only 'chained' runs on the device; the others are usage errors)")
     p.add_argument("--dtype", choices=sorted(DTYPES), default="i32")
     p.add_argument("--op", choices=OPERATOR_NAMES, default="add")
     p.add_argument("--n", action="append", type=int, metavar="N", help="input length; repeatable")
     p.add_argument("--n-preset", choices=["paper"], help="the published sizes (32M..512M)")
     p.add_argument("--workers", type=int, default=None, help="accepted for compatibility (grid = resident CTAs)")
+    p.add_argument("--warp-width", type=int, default=32, metavar="W",
+                   help="accepted for compatibility: power of two in [2, 64] (the device warp is 32)")
+    p.add_argument("--k", type=int, default=8, metavar="K", help="accepted for compatibility (>= 1)")
+    p.add_argument("--warps-per-block", type=int, default=32, metavar="WPB",
+                   help="accepted for compatibility (at most W)")
+    p.add_argument("--block-scan-mode", choices=["vectorized", "warp-model"], default="vectorized",
+                   help="accepted for compatibility")
     p.add_argument("--runs", type=int, default=3)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--in-place", action="store_true")
@@ -90,7 +109,6 @@ def bench_one(args, n: int) -> BenchRecord:
     import torch
 
     from . import scan as S
-    from .records import device_check
     op = make_operator(args.op, args.dtype)
     x = generate_input(n, args.dtype, [args.seed, n])
     cfg = ChainConfig(corrupt_slot=args.inject_slot_fault) if args.inject_slot_fault is not None else None
@@ -107,7 +125,6 @@ def bench_one(args, n: int) -> BenchRecord:
             t0 = time.perf_counter()
             y = fn(prob, cfg)
             times.append(time.perf_counter() - t0)
-        yd = torch.from_numpy(np.ascontiguousarray(y)).cuda()
     else:
         xd = torch.from_numpy(x).cuda()
         yd = xd.clone() if args.in_place else torch.empty_like(xd)
@@ -132,7 +149,8 @@ def bench_one(args, n: int) -> BenchRecord:
     failure = None
     verdict = "skipped"
     if not args.no_validate:
-        failure = device_check(torch.from_numpy(x).cuda(), yd, args.op, args.exclusive)
+        yh = y if args.timing == "host" else yd.cpu().numpy()
+        failure = host_check(x, yh, args.op, args.exclusive)
         verdict = "false" if failure else "true"
     best = min(times)
     es = x.dtype.itemsize
@@ -158,10 +176,26 @@ def main(argv: Optional[List[str]] = None) -> int:
         return _usage(f"subcommand {args.command!r} is not provided (only the benchmark mode is)")
     if args.algo not in ALGORITHMS:
         return _usage(f"algorithm {args.algo!r} has no device implementation; choose from {ALGORITHMS}")
-    if args.workers is not None and args.workers < 1:
-        return _usage(f"--workers must be >= 1, got {args.workers}")
+    workers = args.workers
+    if workers is None and os.environ.get(WORKERS_ENV):
+        # cli.py:99-110: the flag wins, then the environment (validated, but
+        # the device's CTA count is what runs)
+        try:
+            workers = int(os.environ[WORKERS_ENV])
+        except ValueError:
+            return _usage(f"${WORKERS_ENV} must be an integer, got {os.environ[WORKERS_ENV]!r}")
+    if workers is not None and workers < 1:
+        return _usage(f"--workers must be >= 1, got {workers}")
     if args.runs < 1:
         return _usage(f"--runs must be >= 1, got {args.runs}")
+    # WarpGeometry's checks (warp.py:42-82)
+    w = args.warp_width
+    if w < 2 or w > 64 or w & (w - 1):
+        return _usage(f"warp width must be a power of two in [2, 64], got {w}")
+    if args.k < 1:
+        return _usage(f"registers per lane must be >= 1, got {args.k}")
+    if args.warps_per_block < 1 or args.warps_per_block > w:
+        return _usage(f"warps_per_block must be in [1, {w}], got {args.warps_per_block}")
     ns = list(args.n) if args.n else []
     if args.n_preset == "paper":
         ns += PAPER_NS

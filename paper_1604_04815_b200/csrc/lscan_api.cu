@@ -84,6 +84,9 @@ ls_status cuda_fail(cudaError_t e, const char *what) {
 // hooks armed, forced persistent path) runs on the generic kernel
 constexpr int64_t kSplitMinElems = 1 << 20;
 
+// default look-back / exchange probe budget of the multi-GPU kernel
+constexpr int64_t kMultiSpinBudget = int64_t(1) << 28;
+
 // LSCAN_NO_COOP=1: plain launches (lab measurement of the cooperative-launch
 // cost).  The grid never exceeds the co-resident capacity either way.
 bool cooperative_launch() {
@@ -705,7 +708,11 @@ static ls_status scan_multi_impl(ls_op op, ls_dtype dt, const void *x, void *y, 
     p.total_out = total_out;
     p.ws = static_cast<uint8_t *>(ws);
     p.num_tiles = M;
-    p.spin_budget = dbg.spin_budget;
+    // the watchdog is always armed here: a peer GPU that died or never
+    // launches its half of the call must become LS_ERR_LIVENESS in the
+    // workspace (ls_workspace_error), not a hang of every other GPU.  The
+    // default budget is large (each probe sleeps; ~30 s or more of waiting)
+    p.spin_budget = dbg.spin_budget > 0 ? dbg.spin_budget : kMultiSpinBudget;
     p.corrupt_tile = dbg.corrupt;
     p.protocol_checks = dbg.protocol;
     p.delay_red_ns = dbg.delay_red_ns;

@@ -55,7 +55,35 @@
 #define LS_LAB_SKIP_LOOKBACK 0
 #endif
 
+// f32 add on packed FADD2 (add.rn.f32x2, sm_100): the reducer folds two
+// elements per instruction (as IADD3 does for integers), and the scanners keep
+// each lane's running prefixes in place and add the row carry to two of them
+// per instruction once the tile prefix arrives.  0 = the scalar forms (lab A/B)
+#ifndef LS_F32_PACKED
+#define LS_F32_PACKED 1
+#endif
+
 namespace lscan {
+
+__device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t v, uint32_t &lo, uint32_t &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+// two independent f32 adds in one instruction (FADD2), round to nearest
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+template <typename T, typename OP>
+__host__ __device__ constexpr bool packed_f32_add() {
+    return LS_F32_PACKED && std::is_same<T, float>::value && OP::code == 0 && !OP::idempotent;
+}
 
 __device__ __forceinline__ void stg128(void *p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -133,6 +161,26 @@ __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
     static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
     if constexpr (ScanFastOp<T, OP>::enabled)
         return reduce_stage_nan<T, OP, TILE_BYTES / 16>(st, lane, 0, TILE_BYTES / (int)sizeof(T));
+    if constexpr (packed_f32_add<T, OP>()) {
+        // four packed accumulators: two FADD2 per 16-byte vector
+        uint64_t acc[4] = {0, 0, 0, 0};
+        const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
+#pragma unroll 2
+        for (int j = 0; j < NV; j += 4) {
+            uint4 q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = lds128(base + (uint32_t)(j + u) * 512u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc[u] = fadd2(acc[u], pack2(q[u].x, q[u].y));
+                acc[u] = fadd2(acc[u], pack2(q[u].z, q[u].w));
+            }
+        }
+        const uint64_t a2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        uint32_t lo, hi;
+        unpack2(a2, lo, hi);
+        return warp_reduce_fixed<T, OP>(__uint_as_float(lo) + __uint_as_float(hi));
+    }
     const T ident = OP::template identity<T>();
     T acc[4] = {ident, ident, ident, ident};
     const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
@@ -713,12 +761,19 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             T rex[VR];   // exclusive prefix of this lane within row j (lane > 0)
             T rtot[VR];  // row totals
             T run;
+            // f32 add (PIP): each lane keeps its chunk's running prefixes in
+            // place (the fold's intermediates), so the carry is added to every
+            // element independently, two per FADD2, once the prefix is known
+            constexpr bool PIP = packed_f32_add<T, OP>() && !EXCL;
             auto row_scans = [&](auto opv) {
                 using O = decltype(opv);
 #pragma unroll
                 for (int j = 0; j < VR; ++j) {
                     T v = r.e[j * RPER];
-                    if constexpr (O::three) {
+                    if constexpr (PIP) {
+#pragma unroll
+                        for (int e = 1; e < RPER; ++e) r.e[j * RPER + e] = v = O::apply(v, r.e[j * RPER + e]);
+                    } else if constexpr (O::three) {
                         // two elements per FMNMX3
 #pragma unroll
                         for (int e = 1; e + 1 < RPER; e += 2) v = O::apply3(v, r.e[j * RPER + e], r.e[j * RPER + e + 1]);
@@ -803,6 +858,19 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                             if (j + 1 < VR) rowpre = O::apply(rowpre, rtot[j]);
                         }
                         if (lane > 0) { acc = has ? O::apply(acc, rex[j]) : rex[j]; has = true; }
+                        if constexpr (PIP) {
+                            // y = carry (+) in-lane prefix; nothing to add before the
+                            // array's first element (no carry: y[0] = x[0] exactly)
+                            if (has) {
+                                const uint64_t cc = pack2(__float_as_uint(acc), __float_as_uint(acc));
+#pragma unroll
+                                for (int q = 0; q < RPER / 4; ++q) {
+                                    uint4 &w = r.q[j * VW + q];
+                                    unpack2(fadd2(cc, pack2(w.x, w.y)), w.x, w.y);
+                                    unpack2(fadd2(cc, pack2(w.z, w.w)), w.z, w.w);
+                                }
+                            }
+                        } else {
 #pragma unroll
                         for (int e = 0; e < RPER; ++e) {
                             const T v = r.e[j * RPER + e];
@@ -814,6 +882,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                                 acc = first ? v : O::apply(acc, v);
                                 r.e[j * RPER + e] = acc;
                             }
+                        }
                         }
                     }
                     // 16-byte vector index of the lane's chunk in this row

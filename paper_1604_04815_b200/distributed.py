@@ -57,30 +57,99 @@ def cuda_ops(op: str = "add") -> ShardOps:
                     carry=lambda t, r: S.carry_from_totals(t, r, op=op), scan=_scan)
 
 
+def _gather_totals(total: torch.Tensor, world: int, group) -> torch.Tensor:
+    totals = torch.empty(world, dtype=total.dtype, device=total.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(totals, total.reshape(1), group=group)
+    else:
+        dist.all_gather(list(totals.split(1)), total.reshape(1), group=group)
+    return totals
+
+
 def sharded_scan(shard: torch.Tensor, *, exclusive: bool = False, group=None,
                  ops: Optional[ShardOps] = None, out: Optional[torch.Tensor] = None,
-                 op: str = "add") -> torch.Tensor:
+                 op: str = "add", scan_events=None) -> torch.Tensor:
     """Scan this rank's shard as part of the global array (ranks in order).
 
     Every rank must call this collectively.  Returns this rank's slice of the
-    global scan."""
+    global scan.  ``scan_events``: an optional (start, end) pair of CUDA
+    events recorded around the carried scan on the current stream (bench.py
+    times the dominant kernel inside the step with them)."""
     ops = ops or cuda_ops(op)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    total = ops.reduce(shard).reshape(1)
-    totals = torch.empty(world, dtype=shard.dtype, device=shard.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(totals, total, group=group)
-    else:
-        parts = list(totals.split(1))
-        dist.all_gather(parts, total, group=group)
+    totals = _gather_totals(ops.reduce(shard), world, group)
     carry = ops.carry(totals, rank) if rank > 0 else None
-    if out is None:
-        return ops.scan(shard, carry, exclusive)
-    res = ops.scan(shard, carry, exclusive, out=out)
-    if res is not out:
-        out.copy_(res)
+    if scan_events is not None:
+        scan_events[0].record()
+    res = ops.scan(shard, carry, exclusive) if out is None else ops.scan(shard, carry, exclusive, out=out)
+    if scan_events is not None:
+        scan_events[1].record()
+    if out is None or res is out:
+        return res
+    out.copy_(res)
     return out
+
+
+def sharded_scan_host(xh: torch.Tensor, yh: torch.Tensor, *, exclusive: bool = False, group=None,
+                      op: str = "add", chunk_elems: int = 1 << 23,
+                      device_buf: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """End to end from host memory for contiguous shards: this rank's shard
+    ``xh`` (pinned CPU tensor) -> ``yh``.  Collective.
+
+    The carry of a contiguous shard is known only once every lower rank has
+    its whole shard on the device and reduced, so the pipeline has two
+    overlapped halves around the one exchange:
+
+    1. copy-in chunk by chunk (stream ``s_in``), each landed chunk reduced
+       (``s_comp``) into its chunk total — the reduction hides behind PCIe;
+    2. shard total = fold of the chunk totals; all-gather of G scalars;
+       carry = fold of the lower ranks' totals (rank order);
+    3. chunk by chunk: carried scan (``s_comp``; chunk c's carry is chunk
+       c-1's running total) and copy-out (``s_out``) — the scan hides behind
+       PCIe.
+
+    The shard stays resident in HBM between the halves (``device_buf``, or a
+    fresh allocation of the shard's size)."""
+    from . import scan as S
+    n = xh.numel()
+    if yh.numel() != n or xh.dtype != yh.dtype or xh.dim() != 1:
+        raise ValueError("xh and yh must be 1-D host tensors of the same size and dtype")
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d = device_buf if device_buf is not None else torch.empty(n, dtype=xh.dtype, device=dev)
+    if d.numel() < n or d.dtype != xh.dtype:
+        raise ValueError("device_buf must hold the shard")
+    d = d[:n]
+    nch = max(1, (n + chunk_elems - 1) // chunk_elems)
+    bounds = [(c * chunk_elems, min(n, (c + 1) * chunk_elems)) for c in range(nch)]
+    cur = torch.cuda.current_stream(dev)
+    s_in, s_comp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in.wait_stream(cur)
+    s_comp.wait_stream(cur)
+    s_out.wait_stream(cur)
+    part = torch.empty(nch, dtype=xh.dtype, device=dev)
+    run = torch.empty(2, dtype=xh.dtype, device=dev)
+    for c, (lo, hi) in enumerate(bounds):
+        with torch.cuda.stream(s_in):
+            d[lo:hi].copy_(xh[lo:hi], non_blocking=True)
+        s_comp.wait_stream(s_in)
+        with torch.cuda.stream(s_comp):
+            S.reduce(d[lo:hi], part[c:c + 1], op=op)
+    with torch.cuda.stream(s_comp):
+        total = S.reduce(part, op=op)
+        totals = _gather_totals(total, world, group)
+        carry = S.carry_from_totals(totals, rank, op=op) if rank > 0 else None
+        fn = S.exclusive_scan if exclusive else S.inclusive_scan
+        for c, (lo, hi) in enumerate(bounds):
+            cin = carry if c == 0 else run[(c - 1) % 2:(c - 1) % 2 + 1]
+            fn(d[lo:hi], d[lo:hi], carry_in=cin, total_out=run[c % 2:c % 2 + 1], op=op)
+            s_out.wait_stream(s_comp)
+            with torch.cuda.stream(s_out):
+                yh[lo:hi].copy_(d[lo:hi], non_blocking=True)
+    s_out.synchronize()
+    cur.wait_stream(s_comp)
+    return yh
 
 
 # ---------------------------------------------------------------------------

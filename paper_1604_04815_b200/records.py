@@ -1,14 +1,16 @@
 """Benchmark records in the reference's schema (chainscan/bench.py:38-74,
-:215-231) and an on-device result check for the command line.
+:215-231) and the command line's result check.
 
 ``CSV_COLUMNS`` is the reference's pinned column list (test_bench_cli.py:27-32);
 ``EXTENDED_COLUMNS`` appends the device measurements (SURVEY §5 metrics row).
 
-``device_check`` validates a device scan without any CPU scan: integers by
-the exact difference identity y[0] = x[0], y[j] - y[j-1] = x[j] (two's
-complement), max/min against ``torch.cummax``/``cummin`` (exact), float add
-against a float64 device cumsum within the reference envelope
-``FLOAT_EPS_REL * cumsum|x|`` (bench.py:49, :90-114).
+``host_check`` is the reference's validation rule (bench.py:95-114), run on
+the host after timing, with numpy — a checker, not a compute path: the
+sequential fold (``ufunc.accumulate`` with the dtype pinned, wrapping) is
+the reference; integers and max/min must match it exactly — compared as raw
+bits, so a wrong sign of zero or a wrong NaN payload fails (the reference's
+``np.array_equal`` would let a -0/+0 swap through and reject every NaN) —
+and float add must lie inside ``FLOAT_EPS_REL * cumsum|x|`` of it.
 """
 
 from __future__ import annotations
@@ -76,33 +78,41 @@ def format_records(records: Sequence[BenchRecord], fmt: str = "csv", extended: b
     return buf.getvalue()
 
 
-def device_check(x, y, op: str = "add", exclusive: bool = False) -> Optional[str]:
-    """None if the device result y is the scan of x, else a message."""
-    import torch
-    n = x.numel()
+def host_check(x, y, op: str = "add", exclusive: bool = False) -> Optional[str]:
+    """None if y (host array) is the scan of x under the reference's rule
+    (bench.py:95-114, bit-exact for integers and max/min), else a message
+    in the reference's format."""
+    import numpy as np
+    x = np.asarray(x)
+    y = np.asarray(y)
     if y.shape != x.shape:
-        return f"shape mismatch {tuple(y.shape)} vs {tuple(x.shape)}"
+        return f"shape mismatch {y.shape} vs {x.shape}"
+    n = x.size
     if n == 0:
         return None
+    uf = {"add": np.add, "max": np.maximum, "min": np.minimum}[op]
+    with np.errstate(over="ignore", invalid="ignore"):
+        ref = uf.accumulate(x, dtype=x.dtype)
     if exclusive:
-        # exclusive y is the inclusive scan shifted right by one
-        x, y = x[:-1], y[1:]
-        n -= 1
-        if n == 0:
+        from .operators import make_operator
+        ident = make_operator(op, x.dtype).identity
+        ref = np.concatenate([np.array([ident], dtype=x.dtype), ref[:-1]])
+    if x.dtype.kind == "i" or op in ("max", "min"):
+        ub = np.uint32 if x.dtype.itemsize == 4 else np.uint64
+        bad = np.nonzero(ref.view(ub) != y.view(ub))[0]
+        if bad.size == 0:
             return None
-    if op in ("max", "min"):
-        ref = (torch.cummax if op == "max" else torch.cummin)(x, 0).values
-        bad = torch.nonzero(~((ref == y) | (torch.isnan(ref) & torch.isnan(y))))
-    elif not x.dtype.is_floating_point:
-        d = torch.empty_like(x)
-        d[0] = y[0]
-        d[1:] = y[1:] - y[:-1]  # wraps like the scan itself
-        bad = torch.nonzero(d != x)
-    else:
-        ref = torch.cumsum(x.double(), 0)
-        tol = FLOAT_EPS_REL["f32" if x.dtype == torch.float32 else "f64"] * torch.cumsum(x.double().abs(), 0)
-        bad = torch.nonzero((y.double() - ref).abs() > tol)
-    if bad.numel() == 0:
+        j = int(bad[0])
+        return (f"validation failed at index {j}/{n}: expected {ref[j]!r}, got {y[j]!r} "
+                f"(bits {int(ref.view(ub)[j]):#x} vs {int(y.view(ub)[j]):#x}; {bad.size} mismatches)")
+    xs = x[:-1] if exclusive else x
+    env = FLOAT_EPS_REL["f32" if x.dtype.itemsize == 4 else "f64"] * np.add.accumulate(np.abs(xs, dtype=np.float64))
+    if exclusive:
+        env = np.concatenate([[0.0], env])
+    err = np.abs(y.astype(np.float64) - ref.astype(np.float64))
+    bad = np.nonzero(~(err <= env))[0]  # a NaN error is out of the envelope
+    if bad.size == 0:
         return None
-    j = int(bad[0, 0])
-    return f"validation failed at index {j}/{n}: {bad.shape[0]} mismatches"
+    j = int(bad[0])
+    return (f"validation failed at index {j}/{n}: |{y[j]!r} - {ref[j]!r}| = {err[j]:.3e} > tol {env[j]:.3e} "
+            f"({bad.size} indices out of envelope)")

@@ -12,13 +12,14 @@
 #   timing       per-warp-role clock64 totals        (scripts/lab.py --timing)
 #   sleep200 / sleep1000   look-back back-off in ns
 #   evictnormal  evict-normal L2 policy on the TMA loads
+#   nopack       f32 add without the packed FADD2 forms (LS_F32_PACKED=0)
 set -e
 cd "$(dirname "$0")/.."
 declare -A FLAGS=(
   [base]="" [skipred]="-DLS_LAB_SKIP_REDUCE=1" [skiprow]="-DLS_LAB_SKIP_ROWSCAN=1"
   [skipboth]="-DLS_LAB_SKIP_REDUCE=1 -DLS_LAB_SKIP_ROWSCAN=1" [skiplb]="-DLS_LAB_SKIP_LOOKBACK=1"
   [timing]="-DLS_LAB_TIMING=1" [sleep200]="-DLS_LOOKBACK_SLEEP_NS=200" [sleep1000]="-DLS_LOOKBACK_SLEEP_NS=1000"
-  [evictnormal]="-DLS_TMA_EVICT_FIRST=0"
+  [evictnormal]="-DLS_TMA_EVICT_FIRST=0" [nopack]="-DLS_F32_PACKED=0"
 )
 names=("$@")
 [ ${#names[@]} -eq 0 ] && names=("${!FLAGS[@]}")

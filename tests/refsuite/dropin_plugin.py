@@ -4,7 +4,8 @@ Loaded with ``-p dropin_plugin`` before the reference's own test modules are
 collected: it swaps ``chainscan.chained_scan`` — in the package namespace,
 in ``chainscan.chained`` and in ``chainscan.bench`` (whose ``run_algorithm``
 dispatches "chained" to it, bench.py:121-147) — for the GPU drop-in
-``paper_1604_04815_b200.chained_scan``.  The test modules then import the
+``paper_1604_04815_b200.chained_scan``, and ``chainscan.cli.main`` for the
+drop-in's chainscan-compatible command line.  The test modules then import the
 swapped function (``from chainscan import chained_scan``) and run unchanged,
 with the reference's real ``ScanProblem``, ``make_operator`` and
 ``ChainConfig`` objects and its exception classes.  At the end it writes how
@@ -18,6 +19,7 @@ import os
 import chainscan
 import chainscan.bench
 import chainscan.chained
+import chainscan.cli
 
 import paper_1604_04815_b200 as P
 from paper_1604_04815_b200 import _native
@@ -33,6 +35,12 @@ def _dropin(problem, config=None):
 
 for _mod in (chainscan, chainscan.chained, chainscan.bench):
     _mod.chained_scan = _dropin
+
+# the command line: chainscan's CLI tests call chainscan.cli.main(argv); the
+# drop-in's front end (python -m paper_1604_04815_b200) takes its place
+from paper_1604_04815_b200 import cli as _cli  # noqa: E402
+
+chainscan.cli.main = _cli.main
 
 
 def pytest_sessionfinish(session, exitstatus):
