@@ -385,8 +385,9 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
     static_assert(V >= 1 && TILE_BYTES % (SCAN_THREADS * 16) == 0, "whole rows per lane");
     static_assert(!(SHIFT && MULTI), "the shifted window is a single-GPU variant");
     // SHIFT: x is not 16-byte aligned; every tile is loaded as a window of
-    // TILE_BYTES + 16 bytes from the boundary below it (all tiles full: the
-    // host scans the ragged end separately)
+    // TILE_BYTES + 16 bytes from the boundary below it; a window that x does
+    // not fully back (the last tile or two) is loaded as a TMA prefix plus a
+    // plain-loaded ragged vector padded with the identity (see the producer)
     constexpr int STAGE_BYTES = TILE_BYTES + (SHIFT ? 16 : 0);
     static_assert(SCAN_WARPS >= 2 && ws2_threads<SCAN_WARPS, MULTI>() <= 1024, "too many warps");
     using S = Slot<T>;
