@@ -15,32 +15,50 @@ namespace {
 int g_lab_dtype = 0;  // ls_dtype: 0 i32, 1 i64, 2 f32, 3 f64
 
 int g_lab_op = 0;     // 0 add, 1 max
+int g_lab_shift = 0;  // 1: the shifted-window kernel (x misaligned by a whole number of words)
+
+struct LabK {
+    void (*fn)(const ScanParams);
+    int threads;
+    size_t smem;
+};
+
+template <typename T, typename OP, int SW, int TILE, int STAGES, int VW, bool SHIFT>
+LabK labk() {
+    constexpr bool R2 = ws2_red2<T, OP, false, SHIFT>();
+    return {&scan_ws2_kernel<T, OP, SW, TILE, STAGES, false, false, SHIFT, VW>, ws2_threads_x<SW, false, R2>(),
+            scan_ws2_smem_bytes<T, SW, TILE, STAGES, SHIFT, R2>()};
+}
+
+template <typename T, typename OP, int SW, int TILE, int STAGES, int VW>
+LabK pick_s() {
+    return g_lab_shift ? labk<T, OP, SW, TILE, STAGES, VW, true>() : labk<T, OP, SW, TILE, STAGES, VW, false>();
+}
 
 template <typename OP, int SW, int TILE, int STAGES, int VW>
-void (*pick())(const ScanParams) {
+LabK pick() {
     switch (g_lab_dtype) {
-    case 1: return &scan_ws2_kernel<int64_t, OP, SW, TILE, STAGES, false, false, false, VW>;
-    case 2: return &scan_ws2_kernel<float, OP, SW, TILE, STAGES, false, false, false, VW>;
-    case 3: return &scan_ws2_kernel<double, OP, SW, TILE, STAGES, false, false, false, VW>;
-    default: return &scan_ws2_kernel<int32_t, OP, SW, TILE, STAGES, false, false, false, VW>;
+    case 1: return pick_s<int64_t, OP, SW, TILE, STAGES, VW>();
+    case 2: return pick_s<float, OP, SW, TILE, STAGES, VW>();
+    case 3: return pick_s<double, OP, SW, TILE, STAGES, VW>();
+    default: return pick_s<int32_t, OP, SW, TILE, STAGES, VW>();
     }
 }
 
 template <int SW, int TILE, int STAGES, int VW = 1>
 int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t *grid_out) {
     const bool wide = g_lab_dtype == 1 || g_lab_dtype == 3;
-    void (*f)(const ScanParams) =
-        g_lab_op == 1 ? pick<OpMax, SW, TILE, STAGES, VW>() : pick<OpAdd, SW, TILE, STAGES, VW>();
-    // the 64-bit max kernel has a second reducer warp (ws2_red2)
-    const bool red2 = wide && g_lab_op == 1;
-    const size_t smem = scan_ws2_smem_bytes<int64_t, SW, TILE, STAGES, false, true>();
-    const int threads = red2 ? ws2_threads_x<SW, false, true>() : ws2_threads<SW, false>();
+    const LabK k = g_lab_op == 1 ? pick<OpMax, SW, TILE, STAGES, VW>() : pick<OpAdd, SW, TILE, STAGES, VW>();
+    void (*f)(const ScanParams) = k.fn;
+    const size_t smem = k.smem;
+    const int threads = k.threads;
     if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int occ = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)f, threads, smem);
+    if (occ < 1) return -3;
     const int64_t tile_elems = TILE / (wide ? 8 : 4);
     const int64_t M = (n + tile_elems - 1) / tile_elems;
     int64_t G = (int64_t)occ * sms;
@@ -54,6 +72,7 @@ int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t 
     p.num_tiles = M;
     p.corrupt_tile = -1;
     p.stall_tile = -1;
+    p.x_shift = g_lab_shift ? (int)((uintptr_t)x & 15u) : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);
     cfg.blockDim = dim3(threads);
@@ -74,10 +93,15 @@ extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     g_lab_dtype = (flags >> 8) & 3;
     g_lab_op = (flags >> 10) & 1;
+    g_lab_shift = (flags >> 11) & 1;
     switch (cfg) {
     // 32-byte scanner rows (VW = 2) on the production geometries: 32-bit (8, 32 KiB, 6)
     // and 64-bit (12, 48 KiB, 4)
     case 60: return run_ws<8, 32768, 6, 2>(x, y, n, ws, s, grid_out);
+    // round 2: wider 32-byte-row geometries (64-bit max / min, shifted windows)
+    case 62: return run_ws<16, 65536, 3, 2>(x, y, n, ws, s, grid_out);
+    case 63: return run_ws<16, 32768, 6, 2>(x, y, n, ws, s, grid_out);
+    case 64: return run_ws<16, 49152, 4, 2>(x, y, n, ws, s, grid_out);
     case 61: return run_ws<12, 49152, 4, 2>(x, y, n, ws, s, grid_out);
     case 30: return run_ws<16, 32768, 4>(x, y, n, ws, s, grid_out);
     case 31: return run_ws<16, 32768, 5>(x, y, n, ws, s, grid_out);

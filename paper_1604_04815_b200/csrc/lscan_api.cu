@@ -410,7 +410,11 @@ ls_status launch_scan(const DevState &d, ls_op op, ls_dtype dt, const void *x, v
                       const void *carry_in, void *total_out, void *ws, cudaStream_t s, bool excl, bool fast,
                       const DebugCfg &dbg, int x_shift = 0, int head_n = 0) {
     const Launch &L = x_shift ? K(dt).shift[op][excl] : K(dt).scan[op][excl][fast];
-    const int64_t M = num_tiles(dt, n, fast);
+    // tiles of this kernel's own geometry (the shifted-window kernel's may
+    // differ from the aligned one's; every geometry's tile is at least the
+    // generic kernel's, which sizes the workspace)
+    const int64_t te = L.tile_bytes / elem_size(dt);
+    const int64_t M = (n + te - 1) / te;
     const int64_t cap = (int64_t)(x_shift ? d.occ_shift[dt][op][excl] : d.occ[dt][op][excl][fast]) * d.sms;
     int G = (int)std::min<int64_t>(M, cap);
     static const int balanced = [] {
@@ -631,10 +635,13 @@ ls_status ls_reduce(ls_op op, ls_dtype dt, const void *x, int64_t n, void *total
     if (st != LS_OK) return st;
     DevState *d = nullptr;
     if ((st = device_state(&d)) != LS_OK) return st;
-    const int64_t per_cta = (int64_t)kReduceThreads * (16 / es) * 4;
+    const int64_t per_cta = (int64_t)kReduceThreads * (32 / es) * 4;
     int64_t grid = std::min<int64_t>((n + per_cta - 1) / per_cta, (int64_t)d->reduce_occ[dt][op] * d->sms);
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, kMaxGrid));
-    K(dt).launch_reduce(op, x, n, total_out, ws, (int)grid, s);
+    // the head of x (read last by the reverse sweep) stays in L2 for a scan
+    // of the same array right behind: up to half of L2
+    const int64_t keep = std::min<int64_t>(n * es, (int64_t)d->l2_bytes / 2);
+    K(dt).launch_reduce(op, x, n, total_out, ws, (int)grid, keep, s);
     // float max/min add the tie fix-up kernel (lscan_generic.cuh)
     const bool ties = op != LS_OP_ADD && (dt == LS_F32 || dt == LS_F64);
     g_launches.fetch_add(ties ? 2 : 1, std::memory_order_relaxed);

@@ -388,23 +388,89 @@ struct OpNanMinF {
     }
 };
 
+// f64 max / min as one DSETP.MAX / .MIN (+ two selects) instead of the exact
+// form's two DSETPs: identical to numpy's on operands that are neither zeros
+// nor NaNs.  No three-input or NaN-propagating f64 form exists, so the f64
+// reducers keep the exact operator (reduce_nan = false).
+struct OpFastMaxD {
+    static constexpr int code = 1;
+    static constexpr bool idempotent = true;
+    static constexpr bool three = false;
+    __device__ __forceinline__ static double apply(double a, double b) {
+        double r;
+        asm("max.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+        return r;
+    }
+};
+struct OpFastMinD {
+    static constexpr int code = 2;
+    static constexpr bool idempotent = true;
+    static constexpr bool three = false;
+    __device__ __forceinline__ static double apply(double a, double b) {
+        double r;
+        asm("min.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+        return r;
+    }
+};
+
 template <typename T, typename OP>
 struct ScanFastOp {
     static constexpr bool enabled = false;
+    static constexpr bool reduce_nan = false;
     using type = OP;
 };
 template <>
 struct ScanFastOp<float, struct OpMax> {
     static constexpr bool enabled = true;
+    static constexpr bool reduce_nan = true;  // the reducers' NaN-propagating FMNMX(3)
     using type = OpFastMaxF;
     using reduce_type = OpNanMaxF;
 };
 template <>
 struct ScanFastOp<float, struct OpMin> {
     static constexpr bool enabled = true;
+    static constexpr bool reduce_nan = true;
     using type = OpFastMinF;
     using reduce_type = OpNanMinF;
 };
+template <>
+struct ScanFastOp<double, struct OpMax> {
+    static constexpr bool enabled = true;
+    static constexpr bool reduce_nan = false;
+    using type = OpFastMaxD;
+};
+template <>
+struct ScanFastOp<double, struct OpMin> {
+    static constexpr bool enabled = true;
+    static constexpr bool reduce_nan = false;
+    using type = OpFastMinD;
+};
+
+// A lane's registers hold no zero and no NaN (the fast operators' domain).
+// 32-bit words: u = 2 * bits - 1 is 0xffffffff for +-0 and above 0xff000000
+// for a NaN, at most 0xfeffffff otherwise (infinities included); 64-bit
+// elements the same on the doubled bit pattern (NaN above 0xffe0...0)
+template <typename T, int V>
+__device__ __forceinline__ bool fast_domain(const uint4 (&q)[V]) {
+    if constexpr (sizeof(T) == 4) {
+        uint32_t mx0 = 0u, mx1 = 0u;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            mx0 = max(mx0, max(q[i].x + q[i].x - 1u, q[i].y + q[i].y - 1u));
+            mx1 = max(mx1, max(q[i].z + q[i].z - 1u, q[i].w + q[i].w - 1u));
+        }
+        return max(mx0, mx1) <= 0xff000000u;
+    } else {
+        unsigned long long mx = 0ull;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const unsigned long long a = ((unsigned long long)q[i].y << 32) | q[i].x;
+            const unsigned long long b = ((unsigned long long)q[i].w << 32) | q[i].z;
+            mx = max(mx, max(a + a - 1ull, b + b - 1ull));
+        }
+        return mx <= 0xffdfffffffffffffull;
+    }
+}
 
 // Float max/min results depend on the ORDER of equal-comparing operands (-0 /
 // +0) and of NaNs: the sequential fold yields the rightmost of the maximal

@@ -23,6 +23,19 @@ template <>
 struct FastCfg<8> {
     static constexpr int kScanWarps = 12, kTileBytes = 49152, kStages = 4;
 };
+// per element type: f32 takes the 64-bit geometry — 12 scanner warps hide
+// the FADD / FSETP latency chains 8 warps do not (profiles/r2_f32_geometry.json:
+// f32 add 792 -> 812 Gelem/s, f32 max 760 -> 814 at 2^28; i32 stays on 8 warps,
+// where 12 measure 809 -> 795)
+template <typename T>
+struct TypeCfg : FastCfg<sizeof(T)> {};
+template <>
+struct TypeCfg<float> : FastCfg<8> {};
+// the shifted-window kernel (x misaligned): 12 scanner warps / 48 KiB for
+// every type — the word funnel adds scanner work (profiles/r2_shift_geometry.json:
+// i32 add 741 -> 786 Gelem/s with x one element off)
+template <typename T>
+struct ShiftCfg : FastCfg<8> {};
 // the multi-GPU variant carries two more warps (pusher, global chain); the
 // 64-bit single-GPU geometry would then spill (17 warps leave ~100
 // registers a thread), so 64-bit multi-GPU scans use the 32-bit geometry's
@@ -53,7 +66,8 @@ struct DtypeKernels {
     Launch cluster[kNumOps][2][kClusterGeoms];  // [op][exclusive][small, mid, large]: latency kernel (any alignment)
     Launch ordered[kNumOps][2];  // [op][exclusive]: strict left fold, one CTA (the reference's B = 1 path)
     const void *reduce_fn[kNumOps];
-    void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s);
+    void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, int64_t keep_bytes,
+                          cudaStream_t s);
     void (*launch_carry)(int op, const void *totals, int64_t rank, void *carry_out, cudaStream_t s);
     void (*launch_stress)(uint64_t *slots, int64_t count, uint32_t tag, int *writer_done, unsigned long long *stats,
                           int readers, cudaStream_t s);

@@ -212,11 +212,17 @@ constexpr size_t scan_generic_smem_bytes() {
 // Deterministic grid reduction (the per-shard total for the multi-GPU carry
 // exchange): thread-serial over a fixed grid-stride partition, fixed warp and
 // block trees, the last CTA folds the per-CTA partials in index order.
+// 256-bit loads, four in flight per thread (the read-only ceiling probe's
+// access pattern, bench_support/copy_probe.cu).  The sweep runs from the end
+// of x to its start, and the first keep_bytes of x — read last — are loaded
+// evict-last: a carried scan of the same shard right behind it (the
+// contiguous-shard step, distributed.sharded_scan) finds its first tiles in
+// L2 instead of HBM.
 template <typename T, typename OP, int THREADS>
 __global__ void __launch_bounds__(THREADS) reduce_kernel(const T *__restrict__ x, int64_t n, T *total_out,
-                                                         uint8_t *ws) {
+                                                         uint8_t *ws, int64_t keep_bytes) {
     constexpr int NWARPS = THREADS / 32;
-    constexpr int PER_VEC = 16 / (int)sizeof(T);
+    constexpr int PER = 32 / (int)sizeof(T);  // elements per 32-byte chunk
     __shared__ T wsum[NWARPS];
     __shared__ bool last;
     Header *hdr = reinterpret_cast<Header *>(ws);
@@ -226,27 +232,33 @@ __global__ void __launch_bounds__(THREADS) reduce_kernel(const T *__restrict__ x
     const int64_t gstride = (int64_t)gridDim.x * THREADS;
     const T ident = OP::template identity<T>();
 
-    const int64_t mis = (int64_t)(((uintptr_t)x & 15u) / sizeof(T));
-    int64_t head = mis ? (PER_VEC - mis) : 0;
+    const int64_t mis = (int64_t)(((uintptr_t)x & 31u) / sizeof(T));
+    int64_t head = mis ? (PER - mis) : 0;
     if (head > n) head = n;
-    const int64_t nvec = (n - head) / PER_VEC;
-    const int64_t tail0 = head + nvec * PER_VEC;
+    const int64_t nch = (n - head) / PER;
+    const int64_t tail0 = head + nch * PER;
     T acc = ident;
     if (gtid < head) acc = x[gtid];
-    const uint4 *xv = reinterpret_cast<const uint4 *>(x + head);
+    const uint8_t *xc = reinterpret_cast<const uint8_t *>(x + head);
+    const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+    const int64_t keep_ch = keep_bytes / 32;  // chunks [0, keep_ch): evict-last
     int64_t i = gtid;
-    for (; i + 3 * gstride < nvec; i += 4 * gstride) {
-        Regs<T, 4> q;
+    for (; i + 3 * gstride < nch; i += 4 * gstride) {
+        Regs<T, 8> q;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) q.q[u] = __ldcs(xv + i + u * gstride);
+        for (int u = 0; u < 4; ++u) {
+            const int64_t v = nch - 1 - (i + u * gstride);  // reverse sweep
+            ldg256_hint(xc + v * 32, q.q[2 * u], q.q[2 * u + 1], v < keep_ch ? pol_last : pol_first);
+        }
 #pragma unroll
-        for (int j = 0; j < 4 * PER_VEC; ++j) acc = OP::apply(acc, q.e[j]);
+        for (int j = 0; j < 4 * PER; ++j) acc = OP::apply(acc, q.e[j]);
     }
-    for (; i < nvec; i += gstride) {
-        Regs<T, 1> q;
-        q.q[0] = __ldcs(xv + i);
+    for (; i < nch; i += gstride) {
+        Regs<T, 2> q;
+        const int64_t v = nch - 1 - i;
+        ldg256_hint(xc + v * 32, q.q[0], q.q[1], v < keep_ch ? pol_last : pol_first);
 #pragma unroll
-        for (int j = 0; j < PER_VEC; ++j) acc = OP::apply(acc, q.e[j]);
+        for (int j = 0; j < PER; ++j) acc = OP::apply(acc, q.e[j]);
     }
     if (gtid < n - tail0) acc = OP::apply(acc, x[tail0 + gtid]);
 

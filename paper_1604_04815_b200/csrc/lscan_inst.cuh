@@ -12,26 +12,36 @@ namespace lscan {
 // scanner row width of the persistent kernel: 32-byte lane chunks (one
 // 256-bit store, half the warp scans) for every type and operator
 // (profiles/r1_lab_vw.log: f64 add 384 -> 410, f32 max 570 -> 592, i64 add
-// +1 %, 32-bit add +-0 burst and +1.3 % under sustained load)
+// +1 %, 32-bit add +-0 burst and +1.3 % under sustained load) but f32 add,
+// whose 12-warp geometry keeps 16-byte rows (812 vs 804 Gelem/s,
+// profiles/r2_f32_geometry.json)
 template <typename T, typename OP>
 constexpr int ws2_vw() {
-    return 2;
+    return (std::is_same<T, float>::value && OP::code == 0) ? 1 : 2;
 }
 
 template <typename T, typename OP, bool EXCL>
 Launch fast_launch() {
-    using C = FastCfg<sizeof(T)>;
+    using C = TypeCfg<T>;
     constexpr bool R2 = ws2_red2<T, OP, false, false>();
     return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, false, ws2_vw<T, OP>()>,
             ws2_threads_x<C::kScanWarps, false, R2>(),
             scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, false, R2>(), C::kTileBytes, C::kStages};
 }
 
+// the shifted-window kernel's rows: 16-byte for 32-bit add (785 vs 733
+// Gelem/s i32, profiles/r2_shift_geometry.json), else as the aligned kernel.
+// y is (16 * ws2_vw)-byte aligned on this path either way
+template <typename T, typename OP>
+constexpr int shift_vw() {
+    return (sizeof(T) == 4 && OP::code == 0) ? 1 : ws2_vw<T, OP>();
+}
+
 template <typename T, typename OP, bool EXCL>
 Launch shift_launch() {
-    using C = FastCfg<sizeof(T)>;
+    using C = ShiftCfg<T>;
     constexpr bool R2 = ws2_red2<T, OP, false, true>();
-    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true, ws2_vw<T, OP>()>,
+    return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true, shift_vw<T, OP>()>,
             ws2_threads_x<C::kScanWarps, false, R2>(),
             scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true, R2>(), C::kTileBytes, C::kStages};
 }
@@ -89,13 +99,15 @@ void fill_op(DtypeKernels &k) {
 }
 
 template <typename T>
-void launch_reduce_t(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, cudaStream_t s) {
+void launch_reduce_t(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, int64_t keep,
+                     cudaStream_t s) {
     const T *xp = static_cast<const T *>(x);
     T *tp = static_cast<T *>(total_out);
     uint8_t *w = static_cast<uint8_t *>(ws);
-    if (op == OpMax::code) reduce_kernel<T, OpMax, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
-    else if (op == OpMin::code) reduce_kernel<T, OpMin, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
-    else reduce_kernel<T, OpAdd, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w);
+    if (op == OpMax::code) reduce_kernel<T, OpMax, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w, keep);
+    else if (op == OpMin::code)
+        reduce_kernel<T, OpMin, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w, keep);
+    else reduce_kernel<T, OpAdd, kReduceThreads><<<grid, kReduceThreads, 0, s>>>(xp, n, tp, w, keep);
     if constexpr (order_sensitive<T, OpMax>()) {
         // float max/min: the tie fix-up behind it (every block returns at
         // once unless the total is a zero or a NaN)

@@ -54,6 +54,11 @@
 #ifndef LS_LAB_SKIP_LOOKBACK
 #define LS_LAB_SKIP_LOOKBACK 0
 #endif
+// lab: the producer keeps at most this many tile loads in flight (0 = the
+// whole ring) — earlier rounds then land before later ones are requested
+#ifndef LS_LAB_LOOKAHEAD
+#define LS_LAB_LOOKAHEAD 0
+#endif
 
 // f32 add on packed FADD2 (add.rn.f32x2, sm_100): the reducer folds two
 // elements per instruction (as IADD3 does for integers), and the scanners keep
@@ -159,7 +164,7 @@ __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
     constexpr int NV = TILE_BYTES / 16 / 32;  // 16-byte vectors per lane
     constexpr int PER = 16 / (int)sizeof(T);
     static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
-    if constexpr (ScanFastOp<T, OP>::enabled)
+    if constexpr (ScanFastOp<T, OP>::reduce_nan)
         return reduce_stage_nan<T, OP, TILE_BYTES / 16>(st, lane, 0, TILE_BYTES / (int)sizeof(T));
     if constexpr (packed_f32_add<T, OP>()) {
         // four packed accumulators: two FADD2 per 16-byte vector
@@ -203,21 +208,23 @@ __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
 // the same over a shifted window (SHIFT): the stage holds TILE_BYTES + 16
 // bytes from the 16-byte boundary below the tile, whose first `sh` elements
 // belong to the previous tile and whose last vector's first `sh` elements to
-// this one
-template <typename T, typename OP, int TILE_BYTES>
+// this one.  HALF: -1 the whole window; 0 / 1 its lower / upper half (the two
+// reducer warps of RED2: the upper half ends with the window's last vector)
+template <typename T, typename OP, int TILE_BYTES, int HALF = -1>
 __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, int sh) {
-    constexpr int NV = TILE_BYTES / 16 / 32;
+    constexpr int NV = TILE_BYTES / 16 / 32 / (HALF < 0 ? 1 : 2);
     constexpr int PER = 16 / (int)sizeof(T);
-    static_assert(NV % 4 == 0, "tile must hold a multiple of 4 vectors per lane");
+    constexpr int TILE_ELEMS = TILE_BYTES / (int)sizeof(T);
+    static_assert(NV % 4 == 0, "a (half) tile must hold a multiple of 4 vectors per lane");
     const T ident = OP::template identity<T>();
     T acc[4] = {ident, ident, ident, ident};
-    const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
+    const uint32_t base = smem_u32(st) + (HALF == 1 ? (uint32_t)TILE_BYTES / 2u : 0u) + (uint32_t)lane * 16;
 #pragma unroll 2
     for (int j = 0; j < NV; j += 4) {
         Regs<T, 4> r;
 #pragma unroll
         for (int u = 0; u < 4; ++u) r.q[u] = lds128(base + (uint32_t)(j + u) * 512u);
-        if (j == 0 && lane == 0) {
+        if (HALF != 1 && j == 0 && lane == 0) {
 #pragma unroll
             for (int e = 0; e < PER; ++e)
                 if (e < sh) r.e[e] = ident;  // the previous tile's elements
@@ -228,7 +235,7 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
             for (int e = 0; e < PER; ++e) acc[u] = OP::apply(acc[u], r.e[u * PER + e]);
     }
     T a = OP::apply(OP::apply(acc[0], acc[1]), OP::apply(acc[2], acc[3]));
-    if (lane == 0) {
+    if (HALF != 0 && lane == 0) {
         Regs<T, 1> r;
         r.q[0] = lds128(smem_u32(st) + (uint32_t)TILE_BYTES);
 #pragma unroll
@@ -238,7 +245,8 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
     a = warp_reduce_fixed<T, OP>(a);
     if constexpr (order_sensitive<T, OP>())
         if (tie_class(a))
-            return tile_ties<T, OP>(st, lane, a, TILE_BYTES / 16 + 1, sh, sh + TILE_BYTES / (int)sizeof(T));
+            return tile_ties<T, OP>(st, lane, a, TILE_BYTES / 16 + 1, HALF == 1 ? TILE_ELEMS / 2 : sh,
+                                    HALF == 0 ? TILE_ELEMS / 2 : sh + TILE_ELEMS);
     return a;
 }
 
@@ -346,10 +354,14 @@ __host__ __device__ constexpr int ws2_threads() { return (SCAN_WARPS + (MULTI ? 
 // 64-bit max / min: the exact operator is four or five instructions and one
 // reducer warp publishes tile aggregates too late for the look-back (lab:
 // i64 max 340 -> 415 Gelem/s with the reducer pass skipped).  A second
-// reducer warp takes the upper half of each tile.
+// reducer warp takes the upper half of each tile.  LS_SHIFT_RED2 (default
+// on): the shifted-window kernel too, whose reducer also masks the window
+#ifndef LS_SHIFT_RED2
+#define LS_SHIFT_RED2 1
+#endif
 template <typename T, typename OP, bool MULTI, bool SHIFT>
 __host__ __device__ constexpr bool ws2_red2() {
-    return !MULTI && !SHIFT && sizeof(T) == 8 && OP::idempotent;
+    return !MULTI && (!SHIFT || LS_SHIFT_RED2) && sizeof(T) == 8 && OP::idempotent;
 }
 template <int SCAN_WARPS, bool MULTI, bool RED2>
 __host__ __device__ constexpr int ws2_threads_x() { return ws2_threads<SCAN_WARPS, MULTI>() + (RED2 ? 32 : 0); }
@@ -526,7 +538,15 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                 }
             }
         };
-        for (int64_t k = 0; k < STAGES && k < my_tiles; ++k) load_tile(k);
+        if (LS_LAB_LOOKAHEAD > 0 && LS_LAB_LOOKAHEAD < STAGES) {
+            for (int64_t k = 0; k < STAGES && k < my_tiles; ++k) {
+                if (k >= LS_LAB_LOOKAHEAD)
+                    mbar_wait(&full[(k - LS_LAB_LOOKAHEAD) % STAGES], 0u);  // first use of that stage
+                load_tile(k);
+            }
+        } else {
+            for (int64_t k = 0; k < STAGES && k < my_tiles; ++k) load_tile(k);
+        }
         for (int64_t k = 0; k + STAGES < my_tiles; ++k) {
             long long tw = LS_LAB_TIMING ? clock64() : 0;
             mbar_wait(&empty[k % STAGES], (uint32_t)((k / STAGES) & 1));
@@ -539,9 +559,14 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
         for (int64_t k = 0; k < my_tiles; ++k) {
             const int s = (int)(k % STAGES);
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
-            const T a = LS_LAB_SKIP_REDUCE ? ident
-                                           : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES + TILE_BYTES / 2,
-                                                                                 lane);
+            T a = ident;
+            if (!LS_LAB_SKIP_REDUCE) {
+                if constexpr (SHIFT)
+                    a = reduce_stage_shifted<T, OP, TILE_BYTES, 1>(stages + s * STAGE_BYTES, lane,
+                                                                   p.x_shift / (int)sizeof(T));
+                else
+                    a = reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES + TILE_BYTES / 2, lane);
+            }
             __syncwarp();
             if (lane == 0) {
                 red2_val[s] = a;
@@ -559,7 +584,10 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             T a;
             if constexpr (RED2) {
                 // lower half here, upper half from the second reducer, in order
-                a = LS_LAB_SKIP_REDUCE ? ident : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES, lane);
+                a = LS_LAB_SKIP_REDUCE ? ident
+                    : SHIFT ? reduce_stage_shifted<T, OP, TILE_BYTES, 0>(stages + s * STAGE_BYTES, lane,
+                                                                         p.x_shift / (int)sizeof(T))
+                            : reduce_stage<T, OP, TILE_BYTES / 2>(stages + s * STAGE_BYTES, lane);
                 mbar_wait(&red2_ready[s], (uint32_t)((k / STAGES) & 1));
                 a = OP::apply(a, red2_val[s]);
             } else {
@@ -744,20 +772,10 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
 #pragma unroll
                     for (int u = 0; u < VW; ++u) r.q[j * VW + u] = lds128(sbase + (uint32_t)j * ROW_BYTES + 16u * u);
             }
-            // f32 max / min: a warp chunk with no zero and no NaN scans with
-            // one FMNMX per operator (ScanFastOp).  u = 2 * bits - 1 (one
-            // IADD3) is 0xffffffff for +-0 and above 0xff000000 for a NaN,
-            // at most 0xfeffffff otherwise (infinities included)
+            // float max / min: a warp chunk with no zero and no NaN scans with
+            // one FMNMX (f32) / one DSETP.MAX (f64) per operator (ScanFastOp)
             bool fast = false;
-            if constexpr (ScanFastOp<T, OP>::enabled && !SHIFT) {
-                uint32_t mx0 = 0u, mx1 = 0u;
-#pragma unroll
-                for (int i = 0; i < V; ++i) {
-                    mx0 = max(mx0, max(r.q[i].x + r.q[i].x - 1u, r.q[i].y + r.q[i].y - 1u));
-                    mx1 = max(mx1, max(r.q[i].z + r.q[i].z - 1u, r.q[i].w + r.q[i].w - 1u));
-                }
-                fast = __all_sync(0xffffffffu, max(mx0, mx1) <= 0xff000000u);
-            }
+            if constexpr (ScanFastOp<T, OP>::enabled) fast = __all_sync(0xffffffffu, fast_domain<T, V>(r.q));
             // per row j: lane-serial fold of the lane's chunk, inclusive warp scan
             T rex[VR];   // exclusive prefix of this lane within row j (lane > 0)
             T rtot[VR];  // row totals

@@ -24,7 +24,8 @@ CFG_NAMES = {30: "reg16/32K/4", 31: "reg16/32K/5", 32: "reg16/32K/6", 33: "reg16
              35: "reg16/64K/3", 36: "reg16/16K/12", 37: "reg8/16K/12", 38: "reg24/48K/4", 40: "reg12/48K/4",
              41: "reg8/32K/5", 42: "reg8/32K/4", 43: "reg12/48K/3", 44: "reg16/64K/3", 45: "reg4/32K/6",
              46: "reg8/16K/4", 47: "reg4/16K/4", 48: "reg8/16K/3", 49: "reg4/8K/4", 50: "reg8/32K/2",
-             51: "reg4/16K/2", 60: "reg8/32K/6/vw2", 61: "reg12/48K/4/vw2"}
+             51: "reg4/16K/2", 60: "reg8/32K/6/vw2", 61: "reg12/48K/4/vw2", 62: "reg16/64K/3/vw2",
+             63: "reg16/32K/6/vw2", 64: "reg16/48K/4/vw2"}
 
 
 def timeit(fn, reps, warm=3):
@@ -82,6 +83,8 @@ def main():
     ap.add_argument("--product", action="store_true", help="also time the product call (scan.inclusive_scan)")
     ap.add_argument("--timing", action="store_true",
                     help="lab build with -DLS_LAB_TIMING=1: per-phase cycles per tile from the header pad")
+    ap.add_argument("--shift", action="store_true",
+                    help="shifted-window kernel: x one element past a 16-byte boundary, y aligned")
     ap.add_argument("--sustain", type=int, default=0,
                     help="report this many consecutive blocks of --reps calls per config (drift under load)")
     args = ap.parse_args()
@@ -95,17 +98,20 @@ def main():
     code = {"i32": 0, "i64": 1, "f32": 2, "f64": 3}[tok]
     dt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}[tok]
     es = 4 if tok in ("i32", "f32") else 8
+    m = n + (1 if args.shift else 0)
     if dt.is_floating_point:
-        x = torch.rand(n, dtype=dt, device="cuda") * 2 - 1
+        x = torch.rand(m, dtype=dt, device="cuda") * 2 - 1
     else:
-        x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda")
+        x = torch.randint(-2**31, 2**31 - 1, (m,), dtype=dt, device="cuda")
+    if args.shift:
+        x = x[1:]  # 4 or 8 bytes past the allocation's (256-byte) alignment
     y = torch.empty_like(x)
     ws = torch.zeros(L.ls_workspace_bytes(N.LS_I64, n) * 8, dtype=torch.uint8, device="cuda")
     g = ctypes.c_int64(0)
     ref = torch.cumsum(x, 0, dtype=dt) if not dt.is_floating_point else torch.cumsum(x.double(), 0)
     if args.op == "max":
         ref = torch.cummax(x, 0).values
-    flags = (code << 8) | ((1 << 10) if args.op == "max" else 0)
+    flags = (code << 8) | ((1 << 10) if args.op == "max" else 0) | ((1 << 11) if args.shift else 0)
     res = {"n": n, "dtype": str(dt), "lib": args.labso}
     res["torch_copy_gbs"] = round(2 * n * es / (timeit(lambda: y.copy_(x), args.reps) * 1e-3) / 1e9, 1)
     res["torch_cumsum_gelems"] = round(n / (timeit(lambda: torch.cumsum(x, 0, dtype=dt, out=y),

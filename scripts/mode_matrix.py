@@ -15,8 +15,8 @@ from paper_1604_04815_b200 import scan as S  # noqa: E402
 
 def main():
     n = 1 << 28
-    peak, _ = bench.peaks()
-    out = {"n": n, "peak_gbs": peak}
+    peak, src = bench.choose_peak(bench.copy_probes(1 << 31))
+    out = {"n": n, "peak_gbs": peak, "peak_source": src}
     for dt in (torch.int32, torch.int64, torch.float32, torch.float64):
         x = (torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda") if not dt.is_floating_point
              else torch.rand(n, dtype=dt, device="cuda") * 2 - 1)
