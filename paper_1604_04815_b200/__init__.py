@@ -39,7 +39,8 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-level API loaded lazily so the numpy surface imports without torch
-    if name in ("inclusive_scan", "exclusive_scan", "reduce", "reduce_sum", "carry_from_totals", "query_config"):
+    if name in ("inclusive_scan", "exclusive_scan", "reduce", "reduce_sum", "carry_from_totals", "query_config",
+                "release_workspaces"):
         from . import scan
         return getattr(scan, name)
     raise AttributeError(name)
@@ -51,4 +52,5 @@ __all__ = [
     "UnsupportedOperatorError", "WorkspaceError", "chained_exclusive_scan", "chained_scan",
     "default_worker_count", "dtype_token", "make_operator", "parse_dtype", "run_algorithm",
     "inclusive_scan", "exclusive_scan", "reduce", "reduce_sum", "carry_from_totals", "query_config",
+    "release_workspaces",
 ]

@@ -433,6 +433,13 @@ struct ScanFastOp<float, struct OpMin> {
     using type = OpFastMinF;
     using reduce_type = OpNanMinF;
 };
+// f64 fast scans: off by default (LS_F64_FAST_SCAN=1 builds them for the
+// lab): the chunk test costs 64-bit IADD / IMNMX pairs per element and
+// measured slower than the exact DSETP-pair operator it skips
+#ifndef LS_F64_FAST_SCAN
+#define LS_F64_FAST_SCAN 0
+#endif
+#if LS_F64_FAST_SCAN
 template <>
 struct ScanFastOp<double, struct OpMax> {
     static constexpr bool enabled = true;
@@ -445,6 +452,7 @@ struct ScanFastOp<double, struct OpMin> {
     static constexpr bool reduce_nan = false;
     using type = OpFastMinD;
 };
+#endif
 
 // A lane's registers hold no zero and no NaN (the fast operators' domain).
 // 32-bit words: u = 2 * bits - 1 is 0xffffffff for +-0 and above 0xff000000

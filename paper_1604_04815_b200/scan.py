@@ -14,6 +14,7 @@ op ``add``; the numpy-level drop-in with the reference's exact signature is
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 from typing import Dict, Optional, Tuple
 
 import torch
@@ -32,7 +33,13 @@ TORCH_DT = {
 }
 
 _ws_lock = threading.Lock()
-_workspaces: Dict[Tuple[int, int], torch.Tensor] = {}
+# (device index, raw stream) -> workspace, least recently created first.  A
+# caller cycling through many streams would otherwise keep one buffer per
+# stream forever: beyond _WS_CACHE entries the oldest is dropped (the caching
+# allocator hands its memory back only to work ordered after it on the stream
+# it was allocated on, so a scan still in flight there is unaffected).
+_WS_CACHE = 64
+_workspaces: "OrderedDict[Tuple[int, int], torch.Tensor]" = OrderedDict()
 
 
 def dtype_code(dtype: torch.dtype) -> int:
@@ -59,7 +66,20 @@ def workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> t
                 ws = ws[off:off + size]
                 raise_for_status(N.lib().ls_workspace_init(ws.data_ptr(), ws.numel(), stream.cuda_stream))
             _workspaces[key] = ws
+            while len(_workspaces) > _WS_CACHE:
+                _workspaces.popitem(last=False)
         return ws
+
+
+def release_workspaces(device: Optional[torch.device] = None) -> int:
+    """Drop the cached per-stream workspaces (of one device, or all); the
+    next scan on a stream allocates and zeroes a fresh one.  Returns how many
+    were dropped."""
+    with _ws_lock:
+        keys = [k for k in _workspaces if device is None or k[0] == torch.device(device).index]
+        for k in keys:
+            del _workspaces[k]
+    return len(keys)
 
 
 def _check_1d(x: torch.Tensor, what: str = "input") -> None:

@@ -13,6 +13,7 @@
 #   sleep200 / sleep1000   look-back back-off in ns
 #   evictnormal  evict-normal L2 policy on the TMA loads
 #   nopack       f32 add without the packed FADD2 forms (LS_F32_PACKED=0)
+#   f64fast      f64 max/min fast scans on chunks without zeros or NaNs
 #   la1/la2/la3  the producer's first ring fill keeps 1/2/3 tile loads in flight
 set -e
 cd "$(dirname "$0")/.."
@@ -21,6 +22,7 @@ declare -A FLAGS=(
   [skipboth]="-DLS_LAB_SKIP_REDUCE=1 -DLS_LAB_SKIP_ROWSCAN=1" [skiplb]="-DLS_LAB_SKIP_LOOKBACK=1"
   [timing]="-DLS_LAB_TIMING=1" [sleep200]="-DLS_LOOKBACK_SLEEP_NS=200" [sleep1000]="-DLS_LOOKBACK_SLEEP_NS=1000"
   [evictnormal]="-DLS_TMA_EVICT_FIRST=0" [nopack]="-DLS_F32_PACKED=0"
+  [f64fast]="-DLS_F64_FAST_SCAN=1"
   [la1]="-DLS_LAB_LOOKAHEAD=1" [la2]="-DLS_LAB_LOOKAHEAD=2" [la3]="-DLS_LAB_LOOKAHEAD=3"
 )
 names=("$@")

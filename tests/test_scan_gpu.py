@@ -325,3 +325,22 @@ def test_shifted_window_kernel(S1, oracle_lib, tok, xoff):
         check(x, yd.cpu().numpy(), oracle_lib, exclusive=True, what=f"{tok} shifted excl n={n}")
         if tok[0] == "i":
             assert tot.item() == oracle_lib.c_sequential_scan(x)[1]
+
+
+def test_workspace_cache_is_bounded_across_streams(S1):
+    """A caller cycling through many streams keeps at most _WS_CACHE
+    workspaces alive; results stay exact on every stream, and
+    release_workspaces drops them (the next call re-creates one)."""
+    import paper_1604_04815_b200 as P
+    x = torch.arange(1, 5001, dtype=torch.int64, device="cuda")
+    ref = torch.cumsum(x, 0)
+    streams = [torch.cuda.Stream() for _ in range(S1._WS_CACHE + 16)]
+    for s in streams:
+        with torch.cuda.stream(s):
+            y = S1.inclusive_scan(x)
+        s.synchronize()
+        assert torch.equal(y, ref)
+    assert len(S1._workspaces) <= S1._WS_CACHE
+    assert P.release_workspaces() > 0
+    assert len(S1._workspaces) == 0
+    assert torch.equal(S1.inclusive_scan(x), ref)
