@@ -16,6 +16,7 @@ int g_lab_dtype = 0;  // ls_dtype: 0 i32, 1 i64, 2 f32, 3 f64
 
 int g_lab_op = 0;     // 0 add, 1 max
 int g_lab_shift = 0;  // 1: the shifted-window kernel (x misaligned by a whole number of words)
+void *g_lab_timeline = nullptr;  // LS_LAB_TIMELINE builds: per-CTA event times (p.xchg)
 
 struct LabK {
     void (*fn)(const ScanParams);
@@ -73,6 +74,7 @@ int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t 
     p.corrupt_tile = -1;
     p.stall_tile = -1;
     p.x_shift = g_lab_shift ? (int)((uintptr_t)x & 15u) : 0;
+    p.xchg = static_cast<uint8_t *>(g_lab_timeline);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);
     cfg.blockDim = dim3(threads);
@@ -87,7 +89,16 @@ int run_ws(const void *x, void *y, int64_t n, void *ws, cudaStream_t s, int64_t 
 }
 }  // namespace
 
-// flags bits 8..9 select the element type (ls_dtype)
+#ifndef LS_LAB_SMALL
+#define LS_LAB_SMALL 0  // 1: only the production geometries (60, 61, 65) — quick variant builds
+#endif
+
+// LS_LAB_TIMELINE builds: the device buffer (grid x kTimelineWords u64) the
+// kernel writes its per-CTA event times into; nullptr turns the marks off
+extern "C" void ls_lab_set_timeline(void *buf) { g_lab_timeline = buf; }
+
+// flags bits 8..9 select the element type (ls_dtype), bit 10 max, bit 11 the
+// shifted-window kernel
 extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n, void *ws, void *stream,
                           int64_t *grid_out) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -98,11 +109,14 @@ extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n,
     // 32-byte scanner rows (VW = 2) on the production geometries: 32-bit (8, 32 KiB, 6)
     // and 64-bit (12, 48 KiB, 4)
     case 60: return run_ws<8, 32768, 6, 2>(x, y, n, ws, s, grid_out);
+    case 61: return run_ws<12, 49152, 4, 2>(x, y, n, ws, s, grid_out);
+    // f32 add (12 warps, 48 KiB, 16-byte rows)
+    case 65: return run_ws<12, 49152, 4, 1>(x, y, n, ws, s, grid_out);
+#if !LS_LAB_SMALL
     // round 2: wider 32-byte-row geometries (64-bit max / min, shifted windows)
     case 62: return run_ws<16, 65536, 3, 2>(x, y, n, ws, s, grid_out);
     case 63: return run_ws<16, 32768, 6, 2>(x, y, n, ws, s, grid_out);
     case 64: return run_ws<16, 49152, 4, 2>(x, y, n, ws, s, grid_out);
-    case 61: return run_ws<12, 49152, 4, 2>(x, y, n, ws, s, grid_out);
     case 30: return run_ws<16, 32768, 4>(x, y, n, ws, s, grid_out);
     case 31: return run_ws<16, 32768, 5>(x, y, n, ws, s, grid_out);
     case 32: return run_ws<16, 32768, 6>(x, y, n, ws, s, grid_out);
@@ -125,6 +139,7 @@ extern "C" int ls_lab_run(int cfg, int flags, const void *x, void *y, int64_t n,
     case 49: return run_ws<4, 8192, 4>(x, y, n, ws, s, grid_out);
     case 50: return run_ws<8, 32768, 2>(x, y, n, ws, s, grid_out);
     case 51: return run_ws<4, 16384, 2>(x, y, n, ws, s, grid_out);
+#endif
     }
     return -3;
 }

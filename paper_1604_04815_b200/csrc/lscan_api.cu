@@ -155,11 +155,21 @@ struct DevState {
     int occ_shift[4][kNumOps][2] = {};
     int reduce_occ[4][kNumOps] = {};
     int cluster_max = 0;          // largest schedulable cluster of the latency kernel (0: path off)
+    int xl_cluster = 0;           // cluster size of the extra-large geometry (the one placing most blocks)
     int cluster_capacity[kClusterGeoms] = {};  // co-resident clusters of that size per geometry (min over instances)
     int64_t l2_bytes = 0;
 };
 std::mutex g_dev_mu;
 std::deque<DevState> g_dev;  // deque: growing it never moves the states other threads hold
+
+// LSCAN_NO_XL=1: no extra-large cluster geometry (lab A/B)
+bool xl_geometry_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LSCAN_NO_XL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 
 ls_status device_state(DevState **out) {
     int dev = 0;
@@ -228,8 +238,11 @@ ls_status device_state(DevState **out) {
         // the GPCs allow it, else the portable 8; and for several clusters,
         // how many fit at once (the minimum over every instance)
         d.cluster_max = 0;
-        for (int c : {kClusterMax, 8}) {
-            int cap[kClusterGeoms];
+        int caps[2][kClusterGeoms];  // [16, 8][geometry]: co-resident clusters (min over every instance)
+        const int sizes[2] = {kClusterMax, 8};
+        for (int si = 0; si < 2; ++si) {
+            const int c = sizes[si];
+            int *cap = caps[si];
             for (int g = 0; g < kClusterGeoms; ++g) cap[g] = 1 << 30;
             for (int g = 0; g < kClusterGeoms; ++g)
                 for (int dt = 0; dt < 4; ++dt)
@@ -253,9 +266,22 @@ ls_status device_state(DevState **out) {
                             }
                             cap[g] = std::min(cap[g], nc);
                         }
+        }
+        for (int si = 0; si < 2; ++si) {
+            const int *cap = caps[si];
+            // the extra-large geometry is optional (its span is 0 without it)
             if (cap[0] >= 1 && cap[1] >= 1 && cap[2] >= 1) {
-                d.cluster_max = c;
+                d.cluster_max = sizes[si];
                 for (int g = 0; g < kClusterGeoms; ++g) d.cluster_capacity[g] = cap[g];
+                // extra-large tiles: whichever cluster size places the most blocks
+                // at once (GPC packing can favour 8-block clusters there)
+                d.xl_cluster = sizes[si];
+                for (int sj = si; sj < 2; ++sj)
+                    if (caps[sj][3] * sizes[sj] > d.cluster_capacity[3] * d.xl_cluster) {
+                        d.xl_cluster = sizes[sj];
+                        d.cluster_capacity[3] = caps[sj][3];
+                    }
+                if (!xl_geometry_enabled()) d.cluster_capacity[3] = 0;
                 break;
             }
         }
@@ -313,23 +339,28 @@ ls_status identity_fill(ls_op op, ls_dtype dt, void *dst, const void *carry_in, 
 // blocks (carries through DSMEM), several clusters co-resident by a
 // cooperative launch (cluster aggregates through epoch-tagged slots).
 // Geometry g: 0 = small tiles (n fits one cluster of them), 1 = mid tiles
-// (while their clusters fit at once), 2 = large tiles.
+// (while their clusters fit at once), 2 = large tiles, 3 = extra-large tiles
+// (beyond the large ones' co-resident capacity).
+int cluster_size(const DevState &d, int g) { return g == 3 ? d.xl_cluster : d.cluster_max; }
+
 int64_t cluster_span(const DevState &d, ls_dtype dt, int g) {  // elements the geometry covers
     const int64_t te = K(dt).cluster[0][0][g].tile_bytes / elem_size(dt);
-    return te * d.cluster_max * (g == 0 ? 1 : d.cluster_capacity[g]);
+    return te * cluster_size(d, g) * (g == 0 ? 1 : d.cluster_capacity[g]);
 }
 
 int cluster_geometry(const DevState &d, ls_dtype dt, int64_t n) {
     if (n <= cluster_span(d, dt, 0)) return 0;
-    return n <= cluster_span(d, dt, 1) ? 1 : 2;
+    if (n <= cluster_span(d, dt, 1)) return 1;
+    return n <= cluster_span(d, dt, 2) ? 2 : 3;
 }
 
 ls_status launch_cluster(const DevState &d, ls_op op, ls_dtype dt, const void *x, void *y, int64_t n,
                          const void *carry_in, void *total_out, void *ws, cudaStream_t s, bool excl) {
-    const Launch &L = K(dt).cluster[op][excl][cluster_geometry(d, dt, n)];
+    const int g = cluster_geometry(d, dt, n);
+    const Launch &L = K(dt).cluster[op][excl][g];
     const int64_t te = L.tile_bytes / elem_size(dt);
     const int64_t tiles = (n + te - 1) / te;
-    const int C = (int)std::min<int64_t>(tiles, d.cluster_max);
+    const int C = (int)std::min<int64_t>(tiles, cluster_size(d, g));
     const int64_t clusters = (tiles + C - 1) / C;
     ScanParams p{};
     p.x = x;
@@ -375,7 +406,8 @@ int64_t cluster_limit(const DevState &d, ls_dtype dt) {
         const char *e = getenv("LSCAN_CLUSTER_MAX_BYTES");
         return e ? std::max<int64_t>(0, atoll(e)) : kClusterMaxBytes;
     }();
-    const int64_t coresident = std::max(cluster_span(d, dt, 1), cluster_span(d, dt, 2));
+    const int64_t coresident =
+        std::max(std::max(cluster_span(d, dt, 1), cluster_span(d, dt, 2)), cluster_span(d, dt, 3));
     return std::max(cluster_span(d, dt, 0), std::min(coresident, max_bytes / elem_size(dt)));
 }
 

@@ -155,10 +155,14 @@ constexpr int kMaxGrid = 4096;
 //   mid:   8 rows (32 KiB tiles), several co-resident clusters
 //   large: 12 rows (48 KiB tiles), when the mid tiles no longer fit at once
 constexpr int kClusterThreads = 256;
-constexpr int kClusterGeoms = 3;
+constexpr int kClusterGeoms = 4;
 constexpr int kClusterRowsSmall = 4, kClusterMinBlocksSmall = 4;
 constexpr int kClusterRowsMid = 8, kClusterMinBlocksMid = 2;
 constexpr int kClusterRowsLarge = 12, kClusterMinBlocksLarge = 2;
+// extra-large: 16 rows (64 KiB tiles, 2 blocks per SM) — reaches 2^22 32-bit /
+// 2^21 64-bit elements co-resident, where the persistent kernel's round chain
+// costs more than the one-wave cluster exchange
+constexpr int kClusterRowsXL = 16, kClusterMinBlocksXL = 2;
 constexpr int kClusterMax = 16;  // blocks per cluster (non-portable size; 8 where 16 cannot be scheduled)
 constexpr int64_t kClusterMaxBytes = 16ll << 20;  // crossover to the persistent kernel (lab-measured)
 constexpr size_t kSlotBase = sizeof(Header) + (size_t)kMaxGrid * 8;

@@ -63,7 +63,7 @@ struct DtypeKernels {
     Launch multi[kNumOps][2];    // [op][exclusive]: block-cyclic multi-GPU variant of the fast kernel
     int ws2_vw[kNumOps];         // the persistent kernel's scanner row width in vectors (y alignment 16 * vw)
     Launch shift[kNumOps][2];    // [op][exclusive]: x 16 bytes misaligned, y aligned (shifted TMA window)
-    Launch cluster[kNumOps][2][kClusterGeoms];  // [op][exclusive][small, mid, large]: latency kernel (any alignment)
+    Launch cluster[kNumOps][2][kClusterGeoms];  // [op][exclusive][small, mid, large, xl]: latency kernel (any alignment)
     Launch ordered[kNumOps][2];  // [op][exclusive]: strict left fold, one CTA (the reference's B = 1 path)
     const void *reduce_fn[kNumOps];
     void (*launch_reduce)(int op, const void *x, int64_t n, void *total_out, void *ws, int grid, int64_t keep_bytes,

@@ -71,7 +71,9 @@ Launch cluster_launch() {
     // accesses, half the warp scans; -5-6 % per call at 2^18-2^20,
     // profiles/r1_cluster_lab_vw.log); 32-bit and the small geometry: neutral
     // or slower, 16-byte rows
-    constexpr int VW = (sizeof(T) == 8 && V >= 8) ? 2 : 1;
+    // (the extra-large 16-row geometry takes them for every type: 16-byte rows
+    // keep 16 row prefixes live and the 32-bit exclusive forms spilled)
+    constexpr int VW = ((sizeof(T) == 8 && V >= 8) || V >= 16) ? 2 : 1;
     return {&scan_cluster_kernel<T, OP, EXCL, V, kClusterThreads, MINB, VW>, kClusterThreads, 0,
             kClusterThreads * V * 16, 1};
 }
@@ -84,6 +86,8 @@ void fill_op(DtypeKernels &k) {
     k.cluster[OP::code][1][1] = cluster_launch<T, OP, true, kClusterRowsMid, kClusterMinBlocksMid>();
     k.cluster[OP::code][0][2] = cluster_launch<T, OP, false, kClusterRowsLarge, kClusterMinBlocksLarge>();
     k.cluster[OP::code][1][2] = cluster_launch<T, OP, true, kClusterRowsLarge, kClusterMinBlocksLarge>();
+    k.cluster[OP::code][0][3] = cluster_launch<T, OP, false, kClusterRowsXL, kClusterMinBlocksXL>();
+    k.cluster[OP::code][1][3] = cluster_launch<T, OP, true, kClusterRowsXL, kClusterMinBlocksXL>();
     k.scan[OP::code][0][1] = fast_launch<T, OP, false>();
     k.scan[OP::code][1][1] = fast_launch<T, OP, true>();
     k.scan[OP::code][0][0] = generic_launch<T, OP, false>();

@@ -54,11 +54,25 @@
 #ifndef LS_LAB_SKIP_LOOKBACK
 #define LS_LAB_SKIP_LOOKBACK 0
 #endif
-// lab: the producer keeps at most this many tile loads in flight (0 = the
-// whole ring) — earlier rounds then land before later ones are requested
-#ifndef LS_LAB_LOOKAHEAD
-#define LS_LAB_LOOKAHEAD 0
+// The producer's first ring fill keeps at most this many tile loads in
+// flight (0 = the whole ring at once): round 0 then lands before round 1 is
+// requested, so the carry chain starts early instead of behind a ring's
+// worth of interleaved loads (lab, scripts/gpu/r2l.sh: i32 2^24 507 -> 586,
+// 2^26 735 -> 762, 2^28 809 -> 816 Gelem/s; i64 2^23 280 -> 295)
+#ifndef LS_FILL_LOOKAHEAD
+#define LS_FILL_LOOKAHEAD 1
 #endif
+
+// lab: per-CTA event times (%globaltimer ns, 32 ns ticks on B200) into the
+// buffer p.xchg points at (single-GPU lab builds only): [c][0] start, [c][1]
+// end, [c][2 + 8k + e] for the CTA's k-th tile (k < 8): e = 0 data landed
+// (as the reducer sees it), 1 aggregate published, 2 prefix known (look-back
+// warp), 3 stores issued (scanners), 4 look-back started, 5 its first pass of
+// slot loads answered, 6 re-polls (a count) — scripts/timeline_lab.py
+#ifndef LS_LAB_TIMELINE
+#define LS_LAB_TIMELINE 0
+#endif
+constexpr int kTimelineWords = 66;
 
 // f32 add on packed FADD2 (add.rn.f32x2, sm_100): the reducer folds two
 // elements per instruction (as IADD3 does for integers), and the scanners keep
@@ -83,6 +97,12 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     uint64_t r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
+}
+
+__device__ __forceinline__ uint64_t gtimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 template <typename T, typename OP>
@@ -275,7 +295,8 @@ struct LookbackOut {
 template <typename T, typename OP>
 __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, const uint64_t *rnd, int64_t k, int c,
                                                        int G, bool need_r, int64_t r_idx, bool want_own, uint32_t tag,
-                                                       int lane, int64_t spin_budget, Header *hdr, uint32_t where) {
+                                                       int lane, int64_t spin_budget, Header *hdr, uint32_t where,
+                                                       uint64_t *t_first = nullptr) {
     using S = Slot<T>;
     constexpr int U = 5;  // 160 slots per pass covers a 148-SM round
     const T ident = OP::template identity<T>();
@@ -297,6 +318,7 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
             if (need[u]) S::load(agg, first + j, w[u]);
         }
         T val[U];
+        bool first_pass = base == 0;
         while (true) {
             bool ok = true;
             if (r_pending) {
@@ -310,6 +332,8 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
                     else ok = false;
                 }
             }
+            if (LS_LAB_TIMELINE && first_pass && t_first != nullptr) *t_first = gtimer_ns();
+            first_pass = false;
             if (__all_sync(0xffffffffu, ok)) break;
             if (spin_budget > 0 && ++probes > spin_budget) {
                 if (lane == 0) raise_error(hdr, 4u /*LS_ERR_LIVENESS*/, where);
@@ -344,6 +368,90 @@ __device__ __forceinline__ LookbackOut<T> aux_lookback(const uint64_t *agg, cons
     o.sum = fold_finish<T, OP>(acc);
     o.r = r;
     o.own = want_own ? __shfl_sync(0xffffffffu, own, c & 31) : ident;
+    o.polls = polls;
+    return o;
+}
+
+// Round prefixes (single GPU, add): every CTA folds the whole previous round
+// itself (round_lookback) instead of reading the round prefix CTA G-1
+// publishes — no serial hop through one CTA per round (lab, with the fill
+// look-ahead: i32 2^28 816 -> 827, i64 2^27 407 -> 414 Gelem/s).  Not for
+// max / min: float max / min fold each 32-slot chunk with a warp reduction,
+// and the doubled look-back work measured slower there (f32 max 2^28 822 -> 499)
+#ifndef LS_ROUND_FOLD
+#define LS_ROUND_FOLD 1
+#endif
+
+template <typename T>
+struct RoundPair {
+    T prev;  // A[first] (+) ... (+) A[first + n1 - 1]: the whole previous round
+    T cur;   // A[first + n1] (+) ... (+) A[first + n1 + n2 - 1]: this round's tiles before t
+    int polls = 0;
+};
+
+// The look-back of tile t = k*G + c (k >= 1) on a single GPU: the previous
+// round's G aggregates and this round's first c, every load in flight at once
+// (U * 32 >= 2G slots), folded separately in slot order — so every CTA folds
+// round k-1 identically and keeps its own running round prefix R[k-1]; no
+// CTA waits on another's published round prefix (one L2 round trip per
+// tile instead of a serial hop through CTA G-1 per round).
+template <typename T, typename OP, int U>
+__device__ __forceinline__ RoundPair<T> round_lookback(const uint64_t *agg, int64_t first, int n1, int n2,
+                                                       uint32_t tag, int lane, int64_t spin_budget, Header *hdr,
+                                                       uint32_t where) {
+    using S = Slot<T>;
+    const T ident = OP::template identity<T>();
+    const int count = n1 + n2;
+    T a1 = ident, a2 = ident;
+    int64_t probes = 0;
+    int polls = 0;
+    for (int base = 0; base < count; base += 32 * U) {  // one pass while 2G <= 32 U (G <= 160)
+        // raw tagged words only (decoded again for the fold): the 64-bit form
+        // keeps 2U words live, not 2U words and U values
+        uint64_t w[U][S::W];
+        bool need[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * 32 + lane;
+            need[u] = j < count;
+            if (need[u]) S::load(agg, first + j, w[u]);
+        }
+        bool timed_out = false;
+        while (true) {
+            bool ok = true;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (need[u]) {
+                    T v;
+                    if (S::decode(w[u], tag, v)) need[u] = false;
+                    else ok = false;
+                }
+            }
+            if (__all_sync(0xffffffffu, ok)) break;
+            if (spin_budget > 0 && ++probes > spin_budget) {
+                if (lane == 0) raise_error(hdr, 4u /*LS_ERR_LIVENESS*/, where);
+                timed_out = true;  // slots still missing fold as the identity
+                break;
+            }
+            __nanosleep(LS_LOOKBACK_SLEEP_NS);
+            ++polls;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (need[u]) S::load(agg, first + base + u * 32 + lane, w[u]);
+        }
+        // slot order: whole 32-slot chunks, the one straddling n1 split in two
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j0 = base + u * 32, j = j0 + lane;
+            T v = ident;
+            if (j < count && !(timed_out && need[u])) S::decode(w[u], tag, v);
+            if (j0 < n1) a1 = fold_chunk<T, OP>(a1, j < n1 ? v : ident);
+            if (j0 + 32 > n1 && j0 < count) a2 = fold_chunk<T, OP>(a2, j >= n1 ? v : ident);
+        }
+    }
+    RoundPair<T> o;
+    o.prev = fold_finish<T, OP>(a1);
+    o.cur = fold_finish<T, OP>(a2);
     o.polls = polls;
     return o;
 }
@@ -430,6 +538,16 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
     T *y = static_cast<T *>(p.y);
     const int64_t my_tiles = (M - c + G - 1) / G;
     const int64_t full_tiles = p.n / TILE_ELEMS;
+    auto tl_mark = [&](int idx) {  // LS_LAB_TIMELINE only
+        if constexpr (LS_LAB_TIMELINE && !MULTI)
+            if (p.xchg != nullptr && idx < kTimelineWords)
+                reinterpret_cast<volatile uint64_t *>(p.xchg)[(int64_t)c * kTimelineWords + idx] = gtimer_ns();
+    };
+    auto tl_set = [&](int idx, uint64_t v) {  // LS_LAB_TIMELINE only
+        if constexpr (LS_LAB_TIMELINE && !MULTI)
+            if (p.xchg != nullptr && idx < kTimelineWords)
+                reinterpret_cast<volatile uint64_t *>(p.xchg)[(int64_t)c * kTimelineWords + idx] = v;
+    };
 
     if (tid == 0) {
 #pragma unroll
@@ -449,6 +567,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
     // launching right away: its blocks take SMs only as ours exit.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (tid == 0) tl_mark(0);
     const uint32_t tag = call_tag(hdr);
     Header *xhdr = MULTI ? reinterpret_cast<Header *>(p.xchg) : nullptr;
     const uint32_t xtag = MULTI ? call_tag(xhdr) : 0u;
@@ -538,10 +657,10 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                 }
             }
         };
-        if (LS_LAB_LOOKAHEAD > 0 && LS_LAB_LOOKAHEAD < STAGES) {
+        if (LS_FILL_LOOKAHEAD > 0 && LS_FILL_LOOKAHEAD < STAGES) {
             for (int64_t k = 0; k < STAGES && k < my_tiles; ++k) {
-                if (k >= LS_LAB_LOOKAHEAD)
-                    mbar_wait(&full[(k - LS_LAB_LOOKAHEAD) % STAGES], 0u);  // first use of that stage
+                if (k >= LS_FILL_LOOKAHEAD)
+                    mbar_wait(&full[(k - LS_FILL_LOOKAHEAD) % STAGES], 0u);  // first use of that stage
                 load_tile(k);
             }
         } else {
@@ -580,6 +699,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             const int s = (int)(k % STAGES);
             const int64_t t = c + k * G;
             mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+            if (lane == 0) tl_mark(2 + 8 * (int)k);
             if (p.delay_red_ns > 0 && t % 3 == 1) debug_sleep(p.delay_red_ns);
             T a;
             if constexpr (RED2) {
@@ -606,13 +726,14 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                     if (S::decode(w, tag, dummy)) raise_error(hdr, 5u /*LS_ERR_PROTOCOL*/, (uint32_t)t);
                 }
                 if (t != p.stall_tile || p.spin_budget <= 0) S::publish(agg, t, tag, t == p.corrupt_tile ? ident : a);
+                tl_mark(3 + 8 * (int)k);
             }
         }
     } else if (warp == W_AUX) {
         // ----------------------------------------------------------- look-back
         const T *carry_in = static_cast<const T *>(p.carry_in);
         bool have_carry = carry_in != nullptr;
-        T r_prev = have_carry ? *carry_in : ident;  // R[k-1] as known to CTA G-1 (the chain owner)
+        T r_prev = have_carry ? *carry_in : ident;  // R[k-1]: carry (+) head (+) rounds 0 .. k-1 (single GPU)
         if constexpr (!MULTI) {
             // y's head (the few elements before the aligned y this kernel
             // tiles): every CTA folds it into the carry, in sequence order;
@@ -640,16 +761,52 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                     prefix = has ? OP::apply(lb.r, lb.sum) : lb.sum;
                     has = true;
                 }
+            } else if (LS_ROUND_FOLD && OP::code == OpAdd::code) {
+                // prefix(t) = R[k-1] (+) A[kG] (+) ... (+) A[kG+c-1], with R[k-1]
+                // this CTA's own running fold of the whole earlier rounds (no
+                // chain through CTA G-1)
+                const long long tl = LS_LAB_TIMING ? clock64() : 0;
+                T cur = ident;
+                if (LS_LAB_SKIP_LOOKBACK) {
+                } else if (k == 0) {
+                    const LookbackOut<T> lb = aux_lookback<T, OP>(agg, rnd, 0, c, G, false, 0, false, tag, lane,
+                                                                  p.spin_budget, hdr, (uint32_t)t);
+                    cur = lb.sum;
+                    if (LS_LAB_TIMING) lab_polls += lb.polls;
+                } else {
+                    const RoundPair<T> lb = round_lookback<T, OP, 10>(agg, (k - 1) * (int64_t)G, G, c, tag, lane,
+                                                                      p.spin_budget, hdr, (uint32_t)t);
+                    r_prev = have_carry ? OP::apply(r_prev, lb.prev) : lb.prev;
+                    have_carry = true;
+                    cur = lb.cur;
+                    if (LS_LAB_TIMING) lab_polls += lb.polls;
+                }
+                if (LS_LAB_TIMING) {
+                    lab_t[5] += clock64() - tl;  // look-back of one tile
+                    if (c == G - 1) lab_chain += clock64() - tl;
+                }
+                has = have_carry;
+                prefix = r_prev;
+                if (c > 0) {
+                    prefix = has ? OP::apply(prefix, cur) : cur;
+                    has = true;
+                }
             } else {
                 const bool chain = (c == G - 1) && (t + 1 < M);
                 // R[k-1]: the caller's carry in round 0, the chain owner's register,
                 // or the published round slot for everyone else
                 const bool need_r = k > 0 && c != G - 1;
                 const long long tl = LS_LAB_TIMING ? clock64() : 0;
+                uint64_t t_first = 0;
+                if (lane == 0) tl_mark(6 + 8 * (int)k);
                 const LookbackOut<T> lb =
                     LS_LAB_SKIP_LOOKBACK ? LookbackOut<T>{ident, ident, ident, 0}
                                          : aux_lookback<T, OP>(agg, rnd, k, c, G, need_r, k - 1, chain, tag, lane,
-                                                               p.spin_budget, hdr, (uint32_t)t);
+                                                               p.spin_budget, hdr, (uint32_t)t, &t_first);
+                if (lane == 0) {
+                    tl_set(7 + 8 * (int)k, t_first);
+                    tl_set(8 + 8 * (int)k, (uint64_t)lb.polls);
+                }
                 if (LS_LAB_TIMING) {
                     lab_t[5] += clock64() - tl;  // look-back of one tile
                     lab_polls += lb.polls;
@@ -674,6 +831,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                 pre[s] = prefix;
                 pre_has[s] = has ? 1 : 0;
                 mbar_arrive(&pre_ready[s]);
+                tl_mark(4 + 8 * (int)k);
             }
             __syncwarp();
         }
@@ -931,6 +1089,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             } else {
                 fold_store(OP{}, false);
             }
+            if (tid == 0) tl_mark(5 + 8 * (int)k);
             if (LS_LAB_TIMING && tid == 0) {
                 const long long tm4 = clock64();
                 lab_t[0] += tm1 - tm0;  // waiting for the tile's data
@@ -953,6 +1112,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
         }
     }
     __syncthreads();
+    if (tid == 0) tl_mark(1);
     if (tid == 0) {
         if constexpr (MULTI) {
             // the exchange epoch advances with the workspace epoch: the last

@@ -2,7 +2,7 @@
 # Build the persistent-kernel lab library (bench_support/lscan_lab.cu) under the
 # compile-time lab switches of lscan_scan_ws2.cuh, as
 # bench_support/_build/liblscanlab_<name>.so, for scripts/lab.py --labso,
-# scripts/gpu_sustain.sh and scripts/gpu_floatlab.sh.  Runs here (nvcc
+# scripts/gpu/sustain.sh and scripts/gpu/floatlab.sh.  Runs here (nvcc
 # cross-compiles); the .so files travel to the GPU box with the repo.
 #   base         product defaults
 #   skipred      no reducer pass over the stage      (timing only: wrong sums)
@@ -14,7 +14,11 @@
 #   evictnormal  evict-normal L2 policy on the TMA loads
 #   nopack       f32 add without the packed FADD2 forms (LS_F32_PACKED=0)
 #   f64fast      f64 max/min fast scans on chunks without zeros or NaNs
-#   la1/la2/la3  the producer's first ring fill keeps 1/2/3 tile loads in flight
+#   timeline     per-CTA event times (LS_LAB_TIMELINE; production geometries only)
+#   small        production geometries only (cfgs 60, 61, 65)
+#   sla1/2/3     small + look-ahead 1/2/3
+#   la1/la2/la3  the producer's first ring fill keeps 1/2/3 tile loads in flight (product: 1)
+#   schain       small + the round-1 look-back (round chain through CTA G-1, whole first fill at once)
 set -e
 cd "$(dirname "$0")/.."
 declare -A FLAGS=(
@@ -23,7 +27,12 @@ declare -A FLAGS=(
   [timing]="-DLS_LAB_TIMING=1" [sleep200]="-DLS_LOOKBACK_SLEEP_NS=200" [sleep1000]="-DLS_LOOKBACK_SLEEP_NS=1000"
   [evictnormal]="-DLS_TMA_EVICT_FIRST=0" [nopack]="-DLS_F32_PACKED=0"
   [f64fast]="-DLS_F64_FAST_SCAN=1"
-  [la1]="-DLS_LAB_LOOKAHEAD=1" [la2]="-DLS_LAB_LOOKAHEAD=2" [la3]="-DLS_LAB_LOOKAHEAD=3"
+  [timeline]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1" [small]="-DLS_LAB_SMALL=1"
+  [tlrfold]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_ROUND_FOLD=1" [tlla1]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_FILL_LOOKAHEAD=1"
+  [sla1]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=1" [sla2]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=2"
+  [sla3]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=3" [srfold]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1"
+  [srfla1]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1 -DLS_FILL_LOOKAHEAD=1"
+  [la1]="-DLS_FILL_LOOKAHEAD=1" [la2]="-DLS_FILL_LOOKAHEAD=2" [la3]="-DLS_FILL_LOOKAHEAD=3"
 )
 names=("$@")
 [ ${#names[@]} -eq 0 ] && names=("${!FLAGS[@]}")

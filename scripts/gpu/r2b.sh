@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2: f32 add gap vs i32 (geometries, packed FADD2 on/off, per-phase
 # cycles, effective clock) and an ncu capture of the mid-n persistent kernel
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 O=gpurun_out/r2b; mkdir -p $O
 for dt in f32 i32; do
   timeout 300 python scripts/lab.py --dtype $dt --cfgs 60,34,30,32,40,61,33 --labso liblscanlab_base.so --reps 100 > $O/geo_$dt.json 2>&1

@@ -1,6 +1,6 @@
 #!/bin/bash
 # f32 geometry: add / max under the 8-warp and 12-warp geometries, both row widths; i32 control
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 O=gpurun_out/r2c; mkdir -p $O
 for rep in 1 2; do
 timeout 300 python scripts/lab.py --dtype f32 --cfgs 60,34,40,61 --labso liblscanlab_base.so --reps 200 > $O/f32_add_$rep.json 2>&1

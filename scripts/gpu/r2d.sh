@@ -1,7 +1,7 @@
 #!/bin/bash
 # f32 geometry + shifted-window second reducer: GPU tests, misaligned product
 # lab, shifted-window geometry lab, 64-bit max geometry lab
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 O=gpurun_out/r2d; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gputest.log 2>&1; echo tests=$?
 timeout 300 python scripts/misaligned_lab.py > $O/misaligned.log 2>&1

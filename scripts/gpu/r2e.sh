@@ -2,7 +2,7 @@
 # f64 fast max/min, shifted-window geometry + fast path, reduce kernel
 # (256-bit loads, reverse sweep, evict-last head): GPU tests, mode matrix,
 # misaligned lab, shard-step pieces, torchrun world 1; look-ahead lab at mid n
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 O=gpurun_out/r2e; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gputest.log 2>&1; echo tests=$?
 timeout 300 python scripts/misaligned_lab.py > $O/misaligned.log 2>&1

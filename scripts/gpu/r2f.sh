@@ -1,7 +1,7 @@
 #!/bin/bash
 # Re-entry check of HEAD (290c79f kernels): smoke, GPU suite, bench N=1,
 # reference arm, torchrun world 1, mode matrix, misaligned lab
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 O=gpurun_out/r2f; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$?

@@ -1,7 +1,7 @@
 #!/bin/bash
 # f64 max/min with the fast scans off (product) vs on (lab f64fast); mid-n
 # persistent-kernel phase timing and ncu captures of the mid-n kernels
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 O=gpurun_out/r2g; mkdir -p $O
 timeout 400 python scripts/mode_matrix.py > $O/mode_matrix.json 2>&1; echo mm=$?
 timeout 300 python scripts/misaligned_lab.py > $O/misaligned.log 2>&1; echo mis=$?

@@ -25,7 +25,7 @@ CFG_NAMES = {30: "reg16/32K/4", 31: "reg16/32K/5", 32: "reg16/32K/6", 33: "reg16
              41: "reg8/32K/5", 42: "reg8/32K/4", 43: "reg12/48K/3", 44: "reg16/64K/3", 45: "reg4/32K/6",
              46: "reg8/16K/4", 47: "reg4/16K/4", 48: "reg8/16K/3", 49: "reg4/8K/4", 50: "reg8/32K/2",
              51: "reg4/16K/2", 60: "reg8/32K/6/vw2", 61: "reg12/48K/4/vw2", 62: "reg16/64K/3/vw2",
-             63: "reg16/32K/6/vw2", 64: "reg16/48K/4/vw2"}
+             63: "reg16/32K/6/vw2", 64: "reg16/48K/4/vw2", 65: "reg12/48K/4"}
 
 
 def timeit(fn, reps, warm=3):
