@@ -349,7 +349,12 @@ int64_t cluster_span(const DevState &d, ls_dtype dt, int g) {  // elements the g
 }
 
 int cluster_geometry(const DevState &d, ls_dtype dt, int64_t n) {
+    static const int forced = [] {  // LSCAN_CLUSTER_GEOM=1|2|3: lab A/B of the multi-cluster geometries
+        const char *e = getenv("LSCAN_CLUSTER_GEOM");
+        return e ? atoi(e) : 0;
+    }();
     if (n <= cluster_span(d, dt, 0)) return 0;
+    if (forced >= 1 && forced < kClusterGeoms && n <= cluster_span(d, dt, forced)) return forced;
     if (n <= cluster_span(d, dt, 1)) return 1;
     return n <= cluster_span(d, dt, 2) ? 2 : 3;
 }
