@@ -82,7 +82,14 @@ Var var(int v) {
 }
 }  // namespace
 
+namespace {
+void *g_ctl = nullptr;  // LS_LAB_CTIMELINE builds: per-block event times
+int g_csize = 16;       // blocks per cluster
+}  // namespace
+
 extern "C" {
+void lab_set_timeline(void *buf) { g_ctl = buf; }
+void lab_set_cluster_size(int c) { g_csize = c; }
 long long lab_block_elems(int v) {
     const Var w = var(v);
     return (long long)w.threads * w.rows * 16 / w.es;
@@ -94,7 +101,7 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     const Var w = var(v);
     const long long be = lab_block_elems(v);
     const long long tiles = (n + be - 1) / be;
-    const int C = (int)(tiles < 16 ? tiles : 16);
+    const int C = (int)(tiles < g_csize ? tiles : g_csize);
     const long long K = (tiles + C - 1) / C;
     if (C < 1 || (K > 1 && ((v == 4 || v == 5) || !ws))) return -1;
     static bool init[32] = {};  // variants 0..21
@@ -107,6 +114,7 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     p.y = y;
     p.n = n;
     p.ws = static_cast<uint8_t *>(ws);
+    p.xchg = static_cast<uint8_t *>(g_ctl);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(K * C));
     cfg.blockDim = dim3((unsigned)w.threads);

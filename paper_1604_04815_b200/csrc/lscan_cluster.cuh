@@ -27,6 +27,18 @@
 
 namespace lscan {
 
+// lab: per-block event times (%globaltimer ns) into the buffer p.xchg points
+// at (bench_support/cluster_lab.cu builds with -DLS_LAB_CTIMELINE=1; the
+// product never sets p.xchg for this kernel): [b][0] start, [1] loads + row
+// scans done, [2] cluster exchange done, [3] block prefix known, [4] stores
+// issued, [5] warp 0's DSMEM stores issued — held in registers and written
+// at the very end (a global store before the cluster barrier's release would
+// delay it) — scripts/cluster_timeline.py
+#ifndef LS_LAB_CTIMELINE
+#define LS_LAB_CTIMELINE 0
+#endif
+constexpr int kCTimelineWords = 6;
+
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -106,6 +118,11 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t tl_t[kCTimelineWords] = {};
+    auto tl_mark = [&](int idx) {  // LS_LAB_CTIMELINE only
+        if constexpr (LS_LAB_CTIMELINE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t[idx]));
+    };
+    tl_mark(0);
     const uint32_t r = cluster_ctarank();
     const uint32_t C = cluster_nctarank();
     if (C > 1) cluster_arrive_relaxed();  // phase 1: "this CTA is running" (waited on before DSMEM stores)
@@ -162,7 +179,7 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
         T v = d.e[j * RPER];
 #pragma unroll
         for (int e = 1; e < RPER; ++e) v = OP::apply(v, d.e[j * RPER + e]);
-        const T inc = warp_inclusive_scan<T, OP>(v, lane);
+        const T inc = warp_inclusive_scan<T, OP, true>(v, lane);
         if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code)
             rex[j] = OP::apply(inc, (T)(0 - (typename std::make_unsigned<T>::type)v));  // inc - v, exact
         else
@@ -174,11 +191,12 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     if (lane == 0) warp_tot[warp] = run;
     if (C > 1) cluster_wait();  // every CTA of the cluster has started: its shared memory may be written
     __syncthreads();
+    tl_mark(1);
 
     // ---- warp totals -> exclusive warp prefixes; the block aggregate goes to
     //      every later block of the cluster (DSMEM), slot r
     if (warp == 0) {
-        const T wi = warp_inclusive_scan<T, OP>(lane < WARPS ? warp_tot[lane] : ident, lane);
+        const T wi = warp_inclusive_scan<T, OP, true>(lane < WARPS ? warp_tot[lane] : ident, lane);
         const T we = __shfl_up_sync(0xffffffffu, wi, 1);
         if (lane < WARPS) warp_exc[lane] = we;
         const T agg = __shfl_sync(0xffffffffu, wi, WARPS - 1);
@@ -189,9 +207,11 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
             else st_cluster_u64(a, Elem<T>::bits(agg));
         }
         if (lane == 0) block_agg = agg;
+        tl_mark(5);
     }
     if (C > 1) cluster_sync_all();
     else __syncthreads();
+    tl_mark(2);
 
     // ---- block prefix = carry (+) [clusters 0..k-1] (+) [blocks 0..r-1 of this cluster]
     if (warp == 0) {
@@ -243,6 +263,7 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
         }
     }
     __syncthreads();
+    tl_mark(3);
     bool has0 = s_has != 0;
     T pre = s_pre;
     if (warp > 0) {
@@ -301,6 +322,10 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
             }
         }
     }
+    tl_mark(4);
+    if (LS_LAB_CTIMELINE && p.xchg != nullptr && tid == 0)
+        for (int i = 0; i < kCTimelineWords; ++i)
+            reinterpret_cast<uint64_t *>(p.xchg)[(int64_t)blockIdx.x * kCTimelineWords + i] = tl_t[i];
     // the last block to finish records this call's tag as the workspace epoch
     // (relaxed: nothing in this grid reads the epoch again, and the next call
     // starts after this grid has completed)

@@ -324,17 +324,68 @@ __device__ __forceinline__ void store_tile_regs(uint8_t *stage, int tid, Regs<T,
     for (int u = 0; u < V; ++u) sts128(base + (uint32_t)(((u + rot) & (V - 1)) * 16), r.q[u]);
 }
 
-// Hillis-Steele over the 32 lanes (warp.py:93-109), lower-index operand first
-template <typename T, typename OP>
-__device__ __forceinline__ T warp_inclusive_scan(T v, int lane) {
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const T o = __shfl_up_sync(0xffffffffu, v, d);
-        // lanes below d get their own value back; an idempotent operator
-        // absorbs it, so no lane predicate
-        if (OP::idempotent || lane >= d) v = OP::apply(o, v);
-    }
+// v += (the value d lanes down), guarded by the shuffle's own "source lane in
+// range" predicate: one SHFL and one predicated add per level (the C++ form
+// compiles to SHFL + ISETP/SEL + add).  64-bit values shuffle as two halves
+// under the first half's predicate.  IEEE add is commutative, so o + v == v + o.
+__device__ __forceinline__ int32_t shfl_up_add(int32_t v, int d) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
+        : "+r"(v)
+        : "r"(d));
     return v;
+}
+__device__ __forceinline__ float shfl_up_add(float v, int d) {
+    asm("{\n\t.reg .pred p;\n\t.reg .f32 t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n\t@p add.rn.f32 %0, %0, t;\n\t}"
+        : "+f"(v)
+        : "r"(d));
+    return v;
+}
+__device__ __forceinline__ int64_t shfl_up_add(int64_t v, int d) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, tl, th;\n\t.reg .b64 t;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "shfl.sync.up.b32 tl|p, lo, %1, 0, -1;\n\t"
+        "shfl.sync.up.b32 th, hi, %1, 0, -1;\n\t"
+        "mov.b64 t, {tl, th};\n\t@p add.u64 %0, %0, t;\n\t}"
+        : "+l"(v)
+        : "r"(d));
+    return v;
+}
+__device__ __forceinline__ double shfl_up_add(double v, int d) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, tl, th;\n\t.reg .f64 t;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "shfl.sync.up.b32 tl|p, lo, %1, 0, -1;\n\t"
+        "shfl.sync.up.b32 th, hi, %1, 0, -1;\n\t"
+        "mov.b64 t, {tl, th};\n\t@p add.rn.f64 %0, %0, t;\n\t}"
+        : "+d"(v)
+        : "r"(d));
+    return v;
+}
+#ifndef LS_SHFL_PRED_SCAN
+#define LS_SHFL_PRED_SCAN 1
+#endif
+
+// Hillis-Steele over the 32 lanes (warp.py:93-109), lower-index operand first.
+// PRED: add through shfl_up_add (the latency kernel: i64 2^20 7.41 -> 7.09 us,
+// 2^18 5.31 -> 5.12 in the lab; the persistent kernel measured -1 to -2 % with
+// it for 64-bit types and keeps the C++ form)
+template <typename T, typename OP, bool PRED = false>
+__device__ __forceinline__ T warp_inclusive_scan(T v, int lane) {
+    if constexpr (PRED && LS_SHFL_PRED_SCAN && OP::code == 0 && !OP::idempotent) {
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) v = shfl_up_add(v, d);
+        return v;
+    } else {
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const T o = __shfl_up_sync(0xffffffffu, v, d);
+            // lanes below d get their own value back; an idempotent operator
+            // absorbs it, so no lane predicate
+            if (OP::idempotent || lane >= d) v = OP::apply(o, v);
+        }
+        return v;
+    }
 }
 
 // f32 max / min as one FMNMX: identical to numpy's maximum / minimum on

@@ -31,6 +31,7 @@ declare -A FLAGS=(
   [tlrfold]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_ROUND_FOLD=1" [tlla1]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_FILL_LOOKAHEAD=1"
   [sla1]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=1" [sla2]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=2"
   [sla3]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=3" [srfold]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1"
+  [nopred]="-DLS_LAB_SMALL=1 -DLS_SHFL_PRED_SCAN=0"
   [srfla1]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1 -DLS_FILL_LOOKAHEAD=1"
   [la1]="-DLS_FILL_LOOKAHEAD=1" [la2]="-DLS_FILL_LOOKAHEAD=2" [la3]="-DLS_FILL_LOOKAHEAD=3"
 )
