@@ -468,8 +468,21 @@ __host__ __device__ constexpr int ws2_threads() { return (SCAN_WARPS + (MULTI ? 
 #define LS_SHIFT_RED2 1
 #endif
 template <typename T, typename OP, bool MULTI, bool SHIFT>
+// LS_SHIFT_RED2_32: the second reducer for 32-bit max / min in the
+// shifted-window kernel too, whose reducer keeps the exact operator (the
+// aligned kernel's FMNMX3.NAN reducer measured slower there): f32 max with x
+// one element off 554 -> 736, i32 751 -> 823 Gelem/s (lab, scripts/gpu/r2t.sh).
+// LS_SHIFT_RED2_ADD (lab): the same for 64-bit add in the shifted kernel
+#ifndef LS_SHIFT_RED2_32
+#define LS_SHIFT_RED2_32 1
+#endif
+#ifndef LS_SHIFT_RED2_ADD
+#define LS_SHIFT_RED2_ADD 0
+#endif
 __host__ __device__ constexpr bool ws2_red2() {
-    return !MULTI && (!SHIFT || LS_SHIFT_RED2) && sizeof(T) == 8 && OP::idempotent;
+    return !MULTI && (!SHIFT || LS_SHIFT_RED2) &&
+           ((OP::idempotent && (sizeof(T) == 8 || (SHIFT && LS_SHIFT_RED2_32 && sizeof(T) == 4))) ||
+            (SHIFT && LS_SHIFT_RED2_ADD && !OP::idempotent && sizeof(T) == 8));
 }
 template <int SCAN_WARPS, bool MULTI, bool RED2>
 __host__ __device__ constexpr int ws2_threads_x() { return ws2_threads<SCAN_WARPS, MULTI>() + (RED2 ? 32 : 0); }

@@ -32,6 +32,8 @@ declare -A FLAGS=(
   [sla1]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=1" [sla2]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=2"
   [sla3]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=3" [srfold]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1"
   [nopred]="-DLS_LAB_SMALL=1 -DLS_SHFL_PRED_SCAN=0"
+  [shred2_32]="-DLS_LAB_SMALL=1 -DLS_SHIFT_RED2_32=1"
+  [shred2add]="-DLS_LAB_SMALL=1 -DLS_SHIFT_RED2_ADD=1"
   [srfla1]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1 -DLS_FILL_LOOKAHEAD=1"
   [la1]="-DLS_FILL_LOOKAHEAD=1" [la2]="-DLS_FILL_LOOKAHEAD=2" [la3]="-DLS_FILL_LOOKAHEAD=3"
 )
