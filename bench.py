@@ -820,10 +820,22 @@ def cyclic_leg(args, torch, S, dg, xd, tok, tdt, n, es, world, local) -> dict:
     except Exception as e:  # noqa: BLE001 - report, the headline stands
         return {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     y2 = torch.empty_like(xd)
+    # every rank agrees the first fused call went through (the device
+    # watchdog turns a stalled peer into an error instead of a hang) before
+    # any further collective: a rank that failed alone would otherwise leave
+    # the others waiting in the checker's all-gather
+    err = None
     try:
         scanner(xd, y2)
         torch.cuda.synchronize()
         S.check_workspace_error(torch.device("cuda", local))
+    except Exception as e:  # noqa: BLE001
+        err = f"{type(e).__name__}: {str(e)[:200]}"
+    if not all_ranks_true(err is None, dg):
+        del y2
+        scanner.close()
+        return {"error": err or "the fused call failed on another rank"}
+    try:
         val = validate_cyclic(D, scanner, xd, y2, tok)
         dg.barrier()
         steps = min(args.steps, 50)

@@ -41,8 +41,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// LS_MBAR_SUSPEND_NS > 0: try_wait with a suspend-time hint — the waiting
+// thread sleeps in hardware until the phase completes (or the hint expires)
+// instead of re-issuing try_wait / branch in a loop (lab A/B)
+#ifndef LS_MBAR_SUSPEND_NS
+#define LS_MBAR_SUSPEND_NS 0
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "n"(LS_MBAR_SUSPEND_NS > 0 ? LS_MBAR_SUSPEND_NS : 1)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
+    if constexpr (LS_MBAR_SUSPEND_NS > 0) {
+        while (!mbar_try_wait_hint(bar, parity)) {
+        }
+    } else {
+        while (!mbar_try_wait(bar, parity)) {
+        }
     }
 }
 

@@ -34,6 +34,7 @@ declare -A FLAGS=(
   [nopred]="-DLS_LAB_SMALL=1 -DLS_SHFL_PRED_SCAN=0"
   [shred2_32]="-DLS_LAB_SMALL=1 -DLS_SHIFT_RED2_32=1"
   [shred2add]="-DLS_LAB_SMALL=1 -DLS_SHIFT_RED2_ADD=1"
+  [susp]="-DLS_LAB_SMALL=1 -DLS_MBAR_SUSPEND_NS=1000000"
   [srfla1]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1 -DLS_FILL_LOOKAHEAD=1"
   [la1]="-DLS_FILL_LOOKAHEAD=1" [la2]="-DLS_FILL_LOOKAHEAD=2" [la3]="-DLS_FILL_LOOKAHEAD=3"
 )
