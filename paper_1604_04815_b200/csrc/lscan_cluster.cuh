@@ -39,6 +39,32 @@ namespace lscan {
 #endif
 constexpr int kCTimelineWords = 6;
 
+// Lab (LS_CLUSTER_EARLY_AGG=1): with several clusters, the last block of each
+// cluster publishes the cluster aggregate as soon as the other blocks'
+// aggregates have landed in its shared memory (each storer arrives on an
+// mbarrier there, release at cluster scope) instead of after the cluster
+// barrier.  Measured slower: i64 2^17 4.33 -> 5.27 us, 2^20 7.10 -> 8.22,
+// i32 2^21 6.82 -> 7.25 (profiles/r2_cluster_early_agg_ab.jsonl); off
+#ifndef LS_CLUSTER_EARLY_AGG
+#define LS_CLUSTER_EARLY_AGG 0
+#endif
+
+__device__ __forceinline__ void mbar_arrive_remote_cluster(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acquire_cluster(uint64_t *bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -109,6 +135,7 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     __shared__ T block_agg;
     __shared__ T s_pre;                    // carry (+) clusters before this one (+) blocks before this one
     __shared__ int s_has;
+    __shared__ __align__(8) uint64_t agg_bar;  // last block: the other blocks' aggregates have landed
 
     // programmatic dependent launch: the grid may start while the previous
     // kernel in the stream drains; nothing global is touched before this wait
@@ -125,10 +152,16 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     tl_mark(0);
     const uint32_t r = cluster_ctarank();
     const uint32_t C = cluster_nctarank();
-    if (C > 1) cluster_arrive_relaxed();  // phase 1: "this CTA is running" (waited on before DSMEM stores)
     const int64_t b = blockIdx.x;        // tile index
     const int64_t k = b / C;             // cluster index
     const int64_t K = gridDim.x / C;     // clusters in the grid
+    // (not for float max / min: the extra fold's registers spilled the f64 forms)
+    const bool early_agg = LS_CLUSTER_EARLY_AGG && !order_sensitive<T, OP>() && K > 1 && C > 1;
+    if (early_agg && r == C - 1 && tid == 0) {
+        mbar_init(&agg_bar, C - 1);
+        fence_mbar_init();  // visible cluster-wide before the phase-1 barrier completes
+    }
+    if (C > 1) cluster_arrive_relaxed();  // phase 1: "this CTA is running" (waited on before DSMEM stores)
     const T ident = OP::template identity<T>();
     const int64_t t0 = b * TILE_ELEMS;
     int64_t valid = p.n - t0 < TILE_ELEMS ? p.n - t0 : TILE_ELEMS;  // <= 0: a padding block of the last cluster
@@ -193,6 +226,26 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
     __syncthreads();
     tl_mark(1);
 
+    // the earlier clusters' aggregates, folded in cluster order (warp 0)
+    uint64_t *const slots = reinterpret_cast<uint64_t *>(p.ws + kSlotBase);
+    auto read_prev = [&]() -> T {
+        T acc = ident;
+        for (int64_t base = 0; base < k; base += 32) {
+            const int64_t j = base + lane;
+            T v = ident;
+            if (j < k) {
+                uint64_t w[S::W];
+                S::load(slots, j, w);
+                while (!S::decode(w, tag, v)) {
+                    __nanosleep(20);
+                    S::load(slots, j, w);
+                }
+            }
+            acc = fold_chunk<T, OP>(acc, v);
+        }
+        return fold_finish<T, OP>(acc);
+    };
+
     // ---- warp totals -> exclusive warp prefixes; the block aggregate goes to
     //      every later block of the cluster (DSMEM), slot r
     if (warp == 0) {
@@ -205,8 +258,18 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
             const uint32_t a = mapa_shared(local, q);
             if constexpr (sizeof(T) == 4) st_cluster_u32(a, Elem<T>::bits(agg));
             else st_cluster_u64(a, Elem<T>::bits(agg));
+            // the store into the last block, then (release, cluster scope) its arrival
+            if (early_agg && q == C - 1) mbar_arrive_remote_cluster(mapa_shared(smem_u32(&agg_bar), q));
         }
         if (lane == 0) block_agg = agg;
+        if (early_agg && r == C - 1 && lane == 0) {
+            // every other block's aggregate is here: publish the cluster's at once
+            // (the same left fold the blocks of the next clusters expect)
+            mbar_wait_acquire_cluster(&agg_bar, 0u);
+            T pc = Elem<T>::from(cta_agg[0]);
+            for (uint32_t q = 1; q < r; ++q) pc = OP::apply(pc, Elem<T>::from(cta_agg[q]));
+            S::publish(slots, k, tag, OP::apply(pc, agg));
+        }
         tl_mark(5);
     }
     if (C > 1) cluster_sync_all();
@@ -229,24 +292,10 @@ __global__ void __launch_bounds__(THREADS, MINB) scan_cluster_kernel(const ScanP
             // the cluster's aggregate depends on nothing outside the cluster:
             // published at once, so the wait below is one L2 round trip, not
             // a chain (clusters are co-resident: cooperative launch)
-            uint64_t *slots = reinterpret_cast<uint64_t *>(p.ws + kSlotBase);
-            if (r == C - 1 && lane == 0) S::publish(slots, k, tag, hc ? OP::apply(pc, block_agg) : block_agg);
+            if (!early_agg && r == C - 1 && lane == 0)
+                S::publish(slots, k, tag, hc ? OP::apply(pc, block_agg) : block_agg);
             if (k > 0) {
-                T acc = ident;
-                for (int64_t base = 0; base < k; base += 32) {
-                    const int64_t j = base + lane;
-                    T v = ident;
-                    if (j < k) {
-                        uint64_t w[S::W];
-                        S::load(slots, j, w);
-                        while (!S::decode(w, tag, v)) {
-                            __nanosleep(20);
-                            S::load(slots, j, w);
-                        }
-                    }
-                    acc = fold_chunk<T, OP>(acc, v);
-                }
-                const T g = fold_finish<T, OP>(acc);
+                const T g = read_prev();
                 pre = has ? OP::apply(pre, g) : g;
                 has = true;
             }

@@ -16,11 +16,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1604_04815_b200 import scan as S  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
-for dt in (torch.int32, torch.float64):
+for dt in (torch.int32, torch.float32, torch.float64):
     if mode in ("all", "cluster"):
         c = S.query_cluster(dt)
         with S.force_path("cluster"):
-            for n in (5, c["block_elems"] * 3 + 7, c["one_cluster_elems"] + 11, c["mid_max_elems"] + 5):
+            # one cluster, several (mid / large tiles), the extra-large geometry's top
+            for n in (5, c["block_elems"] * 3 + 7, c["one_cluster_elems"] + 11, c["mid_max_elems"] + 5,
+                      c["max_elems"] - 3):
                 for off in (0, 1):
                     x = ((torch.arange(n + 1, dtype=dt, device="cuda") % 7) - 3)[off:off + n]
                     for op in ("add", "max"):
@@ -35,8 +37,11 @@ for dt in (torch.int32, torch.float64):
             # x ends exactly at its allocation's end (no slack to over-read)
             x = ((torch.arange(n + 1, dtype=dt, device="cuda") % 7) - 3)[1:]
             y = S.inclusive_scan(x)
-            assert torch.equal(y, torch.cumsum(x.double(), 0).to(dt)), (dt, n, "shifted")
+            if not dt.is_floating_point or dt == torch.float64:
+                assert torch.equal(y, torch.cumsum(x.double(), 0).to(dt)), (dt, n, "shifted")
             S.exclusive_scan(x)
+            # max with x misaligned, y aligned: the shifted kernel's second reducer (32-bit too)
+            assert torch.equal(S.inclusive_scan(x, op="max"), torch.cummax(x, 0).values), (dt, n, "shifted max")
             # y misaligned the other way: head folded in the kernel
             yb = torch.empty(n + 1, dtype=dt, device="cuda")
             S.inclusive_scan(x, out=yb[1:], op="max")
