@@ -74,6 +74,16 @@ class VirtualGPUs:
             self.raise_(L.ls_workspace_error(self.wss[r][1], self.wss[r][2], self.streams[r].cuda_stream))
         return outs, tots
 
+    def launch(self, x_parts, outs, n, op="add"):
+        """Enqueue one call of n local elements per virtual GPU on its own
+        stream, no synchronisation (the caller arms the watchdog and syncs)."""
+        L, S = self.L, self.S
+        for r in range(self.W):
+            self.raise_(L.ls_inclusive_scan_multi(S.op_code(op), self.dt, x_parts[r].data_ptr(), outs[r].data_ptr(),
+                                                  n, None, None, self.wss[r][1], self.wss[r][2], r, self.W,
+                                                  self.regions[r], self.xbytes, self.peers.data_ptr(), self.grid,
+                                                  self.streams[r].cuda_stream))
+
     def close(self):
         torch.cuda.synchronize()
         for p in self.regions:
@@ -205,3 +215,43 @@ def test_two_pow_33_over_eight_virtual_gpus(env):
             assert y[lo] == (excl[k, r] + x[lo]).to(torch.int32)
     total = order.sum().to(torch.int32)
     assert all(t.item() == total.item() for t in tots)
+
+
+def test_back_to_back_calls_of_unequal_length(env, oracle_lib):
+    """consecutive calls with different n on the same exchange
+    regions (a long call, a short one ending in a partial round, long again),
+    enqueued back to back on every virtual GPU's own stream with no host
+    synchronisation in between, so a fast GPU's next call overlaps a slow
+    GPU's current one: the parity halves of the exchange region are laid out
+    for the region's capacity, not the call's round count."""
+    N, S, raise_ = env
+    W = 3
+    tile = S.query_multi_config(torch.int32, 1 << 20)["tile_elems"]
+    # half the SMs per virtual GPU: each stream may hold its current call and
+    # the next one (launched early through programmatic dependent launch), and
+    # all of them must fit on the one device at once
+    grid = S.query_config(torch.int32, 1 << 20)["sms"] // (2 * W)
+    stripe = grid * tile
+    n_big = 4 * stripe + 17
+    lengths = [n_big, stripe + 3 * tile + 5, n_big, 2 * stripe, 3 * tile + 1, n_big]
+    parts = [oracle_lib.generate_input(n_big, "i32", [g, 7]) for g in range(W)]
+    xd = [torch.from_numpy(p).cuda() for p in parts]
+    v = VirtualGPUs(env, W, torch.int32, n_big, grid)
+    outs = [[torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(W)] for n in lengths]
+    torch.cuda.synchronize()
+    raise_(v.L.ls_debug_config(5_000_000, -1, 0))
+    try:
+        for i, n in enumerate(lengths):
+            v.launch(xd, outs[i], n, op=("add", "max")[i % 2])
+        torch.cuda.synchronize()
+    finally:
+        v.L.ls_debug_config(0, -1, 0)
+    try:
+        for r in range(W):
+            raise_(v.L.ls_workspace_error(v.wss[r][1], v.wss[r][2], v.streams[r].cuda_stream))
+        for i, n in enumerate(lengths):
+            glob = assemble([p[:n] for p in parts], stripe)
+            y = assemble([o.cpu().numpy() for o in outs[i]], stripe)
+            assert np.array_equal(y, oracle_lib.sequential_scan(glob, op=("add", "max")[i % 2])), (i, n)
+    finally:
+        v.close()

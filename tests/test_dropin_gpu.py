@@ -159,3 +159,30 @@ def test_c8_throughput_over_sequential(oracle_lib):
     torch.cuda.synchronize()
     t_dev = (time.perf_counter() - t0) / 10
     assert t_seq / t_dev >= 100, (t_seq, t_dev)
+
+
+@pytest.mark.parametrize("tok", ["i32", "i64"])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_ramped_chunk_schedule(oracle_lib, tok, pinned):
+    """The host pipeline's head / tail chunks ramp from chunk/32 up to the full
+    32 MiB chunk and back (lscan_host.cu chunk_schedule): exact across the
+    switch-over size (2 * ramp + chunk) and well past it, inclusive and
+    exclusive, pinned (direct DMA) and pageable (staged)."""
+    es = 4 if tok == "i32" else 8
+    chunk = (32 << 20) // es
+    ramp = sum(chunk >> s for s in range(1, 6))
+    op = P.make_operator("add", tok)
+    for n in (2 * ramp + chunk, 2 * ramp + chunk + 1, 3 * chunk + 2 * ramp + 777):
+        x = oracle_lib.generate_input(n, tok, [4, n])
+        if pinned:
+            tdt = torch.int32 if tok == "i32" else torch.int64
+            xp = torch.empty(n, dtype=tdt).pin_memory()
+            yp = torch.empty(n, dtype=tdt).pin_memory()
+            xp.numpy()[:] = x
+            xs, ys = xp.numpy(), yp.numpy()
+        else:
+            xs, ys = x, np.empty_like(x)
+        y = P.chained_scan(P.ScanProblem(xs, op, out=ys))
+        assert np.array_equal(y, oracle_lib.c_sequential_scan(x)[0]), (tok, n, pinned)
+        ye = P.chained_exclusive_scan(P.ScanProblem(xs, op, out=ys))
+        assert np.array_equal(ye, oracle_lib.c_sequential_scan(x, exclusive=True)[0]), (tok, n, pinned)
