@@ -15,6 +15,7 @@
 //    16..21: 32-byte lane rows (VW = 2): 256x4, 256x8 minb2, i64 256x4, i64 256x8 minb2,
 //            i64 256x12 minb2, 256x12 minb2
 //    22..24: i64, 512 threads, VW = 2: 4 rows minb2, 8 rows minb1, 6 rows minb1
+//    25, 26: f64 256 x 8 minb2, 256 x 12 minb2 (the product mid / large geometries)
 //   lab_block_elems(variant) -> elements per block (int32)
 #include <cuda_runtime.h>
 
@@ -77,7 +78,10 @@ Var var(int v) {
     case 21: return {&scan_cluster_kernel<int32_t, OpAdd, false, 12, 256, 2, 2>, 256, 12};
     case 22: return {&scan_cluster_kernel<int64_t, OpAdd, false, 4, 512, 2, 2>, 512, 4, 8};
     case 23: return {&scan_cluster_kernel<int64_t, OpAdd, false, 8, 512, 1, 2>, 512, 8, 8};
-    default: return {&scan_cluster_kernel<int64_t, OpAdd, false, 6, 512, 1, 2>, 512, 6, 8};
+    case 24: return {&scan_cluster_kernel<int64_t, OpAdd, false, 6, 512, 1, 2>, 512, 6, 8};
+    // f64 on the product mid / large geometries (as 19 / 20 for i64)
+    case 25: return {&scan_cluster_kernel<double, OpAdd, false, 8, 256, 2, 2>, 256, 8, 8};
+    default: return {&scan_cluster_kernel<double, OpAdd, false, 12, 256, 2, 2>, 256, 12, 8};
     }
 }
 }  // namespace
@@ -104,7 +108,7 @@ int lab_cluster(int v, const void *x, void *y, long long n, void *ws, int coop, 
     const int C = (int)(tiles < g_csize ? tiles : g_csize);
     const long long K = (tiles + C - 1) / C;
     if (C < 1 || (K > 1 && ((v == 4 || v == 5) || !ws))) return -1;
-    static bool init[32] = {};  // variants 0..21
+    static bool init[32] = {};  // variants 0..26
     if (!init[v]) {
         cudaFuncSetAttribute((const void *)w.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         init[v] = true;

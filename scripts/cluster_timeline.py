@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--csize", type=int, default=16)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--lib", default="libclusterlab_tl.so")
+    ap.add_argument("--data", default="int", choices=["int", "unit", "fullint"],
+                    help="int: small integers; unit: U[-1,1] (floats); fullint: full-range ints")
     a = ap.parse_args()
     L = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", a.lib))
     L.lab_cluster.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
@@ -44,10 +46,15 @@ def main():
     L.lab_set_cluster_size.argtypes = [ctypes.c_int]
     L.lab_set_cluster_size(a.csize)
     be = L.lab_block_elems(a.variant)  # elements of the variant's own type
-    es = 8 if a.variant in (8, 9, 10, 11, 13, 14, 18, 19, 20, 22, 23, 24) else 4
-    dt = torch.int64 if es == 8 else torch.int32
+    es = 8 if a.variant in (8, 9, 10, 11, 13, 14, 18, 19, 20, 22, 23, 24, 25, 26) else 4
+    dt = torch.float64 if a.variant in (25, 26) else (torch.int64 if es == 8 else torch.int32)
     n = a.n
-    x = torch.randint(-1000, 1000, (n,), dtype=dt, device="cuda")
+    if a.data == "unit":
+        x = torch.rand(n, dtype=dt, device="cuda") * 2 - 1
+    elif a.data == "fullint":
+        x = torch.randint(torch.iinfo(dt).min, torch.iinfo(dt).max, (n,), dtype=dt, device="cuda")
+    else:
+        x = torch.randint(-1000, 1000, (n,), device="cuda").to(dt)  # integer-valued: f64 sums exact
     y = torch.empty_like(x)
     ws = torch.zeros(1 << 22, dtype=torch.uint8, device="cuda")
     blocks = -(-n // be)
@@ -60,9 +67,12 @@ def main():
 
     L.lab_set_timeline(None)
     us = graph_ms(step, 50) * 1e3
-    ok = bool(torch.equal(y, torch.cumsum(x, 0, dtype=dt)))
+    if a.data == "unit":
+        ok = bool(((y - torch.cumsum(x, 0)).abs() <= 1e-9 * torch.cumsum(x.abs(), 0) + 1e-12).all())
+    else:
+        ok = bool(torch.equal(y, torch.cumsum(x, 0, dtype=dt)))  # exact for integer-valued f64 too
     if a.lib != "libclusterlab_tl.so":  # a build without the marks: graph time only
-        print(json.dumps({"variant": a.variant, "n": n, "csize": a.csize, "lib": a.lib,
+        print(json.dumps({"variant": a.variant, "n": n, "csize": a.csize, "lib": a.lib, "data": a.data,
                           "graph_us_no_marks": round(us, 3), "exact": ok}))
         return
     L.lab_set_timeline(tl.data_ptr())
@@ -71,7 +81,7 @@ def main():
     torch.cuda.synchronize()
     v = tl[:blocks * WORDS].view(blocks, WORDS).cpu().tolist()
     t0 = min(r[0] for r in v)
-    out = {"variant": a.variant, "n": n, "csize": a.csize, "blocks": blocks, "graph_us_no_marks": round(us, 3),
+    out = {"variant": a.variant, "n": n, "csize": a.csize, "data": a.data, "blocks": blocks, "graph_us_no_marks": round(us, 3),
            "exact": ok}
     for e, name in enumerate(EVENTS):
         vals = [(r[e] - t0) / 1e3 for r in v]
