@@ -659,6 +659,17 @@ def run_ours(args):
         out["sustained"] = {"value": round(total_elems / (mss * 1e-3) * 1e-9, 2), "steps": k,
                             "seconds": round(k * mss * 1e-3, 2), "ms_per_step": round(mss, 5),
                             "clocks": sampler.summary(t0, time.time())}
+        if not use_dist:
+            # the same ~1 s of back-to-back device copies of the same bytes
+            # (read x, write y): the sustained ceiling the scan is held to
+            kc = max(10, int(math.ceil(1.0 / (2 * n * es / 6.5e12))))
+            t0 = time.time()
+            msc = time_device(lambda: yd.copy_(xd), kc, 3, stream, dg)
+            cgbs = 2 * n * es / (msc * 1e-3) / 1e9
+            sgbs = 2 * n * es / (mss * 1e-3) / 1e9
+            out["sustained"].update({"gbs": round(sgbs, 1), "copy_gbs": round(cgbs, 1),
+                                     "frac_of_sustained_copy": round(sgbs / cgbs, 4),
+                                     "copy_clocks": sampler.summary(t0, time.time())})
 
     # ---- e2e through the public API with host buffers
     if not args.no_e2e and xh is not None:
