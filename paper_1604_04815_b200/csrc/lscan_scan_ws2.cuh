@@ -74,6 +74,12 @@
 #endif
 constexpr int kTimelineWords = 66;
 
+// lab: the scanners' row scans through the predicated-shuffle add
+// (shfl_up_add, as the latency kernel); measured -1 to -2 % for 64-bit types
+#ifndef LS_WS2_PRED_SCAN
+#define LS_WS2_PRED_SCAN 0
+#endif
+
 // f32 add on packed FADD2 (add.rn.f32x2, sm_100): the reducer folds two
 // elements per instruction (as IADD3 does for integers), and the scanners keep
 // each lane's running prefixes in place and add the row carry to two of them
@@ -977,7 +983,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                         rtot[j] = v;
                         continue;
                     }
-                    const T inc = warp_inclusive_scan<T, O>(v, lane);
+                    const T inc = warp_inclusive_scan<T, O, LS_WS2_PRED_SCAN != 0>(v, lane);
                     if constexpr (std::is_integral<T>::value && OP::code == OpAdd::code) {
                         // integer add: the exclusive prefix is inclusive - own value,
                         // exact modulo 2^width, one shuffle fewer per row (+1-2 % i64)
