@@ -276,6 +276,15 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
     return a;
 }
 
+// the same with the shift known at compile time: pure register renaming
+template <int SW>
+__device__ __forceinline__ uint4 funnel_words_c(uint4 a, uint4 b) {
+    static_assert(SW >= 1 && SW <= 3, "a whole number of words inside one vector");
+    if constexpr (SW == 1) return make_uint4(a.y, a.z, a.w, b.x);
+    else if constexpr (SW == 2) return make_uint4(a.z, a.w, b.x, b.y);
+    else return make_uint4(a.w, b.x, b.y, b.z);
+}
+
 // 16 bytes starting `sw` 32-bit words into a (continuing into b), sw in 1..3
 __device__ __forceinline__ uint4 funnel_words(uint4 a, uint4 b, int sw) {
     uint4 r;
@@ -931,17 +940,30 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             if constexpr (SHIFT) {
                 // logical vector v = window bytes [16v + shift, +16): two aligned
                 // reads and a word funnel (x is element-aligned, so the shift is
-                // a whole number of 32-bit words)
-                const int sw = p.x_shift >> 2;
+                // a whole number of 32-bit words).  The shift is made a compile-
+                // time constant — always 2 words for 64-bit elements, one of three
+                // load loops for 32-bit ones — so the funnel is register renaming
+                // instead of branches and predicated moves per vector
+                auto load_rows = [&](auto swc) {
+                    constexpr int SW = decltype(swc)::value;
 #pragma unroll
-                for (int j = 0; j < VR; ++j) {
-                    uint4 a = lds128(sbase + (uint32_t)j * ROW_BYTES);
+                    for (int j = 0; j < VR; ++j) {
+                        uint4 a = lds128(sbase + (uint32_t)j * ROW_BYTES);
 #pragma unroll
-                    for (int u = 0; u < VW; ++u) {
-                        const uint4 b = lds128(sbase + (uint32_t)j * ROW_BYTES + 16u * (u + 1));
-                        r.q[j * VW + u] = funnel_words(a, b, sw);
-                        a = b;
+                        for (int u = 0; u < VW; ++u) {
+                            const uint4 b = lds128(sbase + (uint32_t)j * ROW_BYTES + 16u * (u + 1));
+                            r.q[j * VW + u] = funnel_words_c<SW>(a, b);
+                            a = b;
+                        }
                     }
+                };
+                if constexpr (sizeof(T) == 8) {
+                    load_rows(std::integral_constant<int, 2>{});
+                } else {
+                    const int sw = p.x_shift >> 2;
+                    if (sw == 1) load_rows(std::integral_constant<int, 1>{});
+                    else if (sw == 2) load_rows(std::integral_constant<int, 2>{});
+                    else load_rows(std::integral_constant<int, 3>{});
                 }
             } else {
 #pragma unroll
