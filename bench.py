@@ -769,8 +769,8 @@ def e2e_leg(args, torch, S, xh, xd, yd, tok, tdt, n, es, world, rank, dg, scanne
 
         def host_step():
             sharded_scan_host(xp, yp, device_buf=yd)
-        api = ("per rank: distributed.sharded_scan_host(pinned shard): chunked copy-in + reduce, all-gather, "
-               "chunked carried scan + copy-out")
+        api = ("per rank: distributed.sharded_scan_host(pinned shard): copy-in, reduce, all-gather of the "
+               "shard totals, carried scan, copy-out (the copy-out waits for every rank's copy-in)")
     else:
         def host_step():
             scanner.scan_host(xp, yp)

@@ -92,25 +92,22 @@ def sharded_scan(shard: torch.Tensor, *, exclusive: bool = False, group=None,
 
 
 def sharded_scan_host(xh: torch.Tensor, yh: torch.Tensor, *, exclusive: bool = False, group=None,
-                      op: str = "add", chunk_elems: int = 1 << 23,
+                      op: str = "add", chunk_elems: int = 0,
                       device_buf: Optional[torch.Tensor] = None) -> torch.Tensor:
     """End to end from host memory for contiguous shards: this rank's shard
     ``xh`` (pinned CPU tensor) -> ``yh``.  Collective.
 
     The carry of a contiguous shard is known only once every lower rank has
-    its whole shard on the device and reduced, so the pipeline has two
-    overlapped halves around the one exchange:
-
-    1. copy-in chunk by chunk (stream ``s_in``), each landed chunk reduced
-       (``s_comp``) into its chunk total — the reduction hides behind PCIe;
-    2. shard total = fold of the chunk totals; all-gather of G scalars;
-       carry = fold of the lower ranks' totals (rank order);
-    3. chunk by chunk: carried scan (``s_comp``; chunk c's carry is chunk
-       c-1's running total) and copy-out (``s_out``) — the scan hides behind
-       PCIe.
-
-    The shard stays resident in HBM between the halves (``device_buf``, or a
-    fresh allocation of the shard's size)."""
+    its whole shard on the device and reduced, so the copy-out cannot start
+    before every copy-in has finished: the call is one H2D DMA of the shard,
+    ``ls_reduce`` (~0.15 ms per GiB, hidden in the copy's tail), the
+    all-gather of G scalars, the carried scan (~0.33 ms per GiB) and one D2H
+    DMA — two PCIe transfers in sequence, each at the link's one-way rate
+    (the block-cyclic ``CyclicScan.scan_host`` overlaps both directions
+    instead).  ``chunk_elems`` is accepted for compatibility and unused: the
+    earlier chunked form spent its time in per-chunk launches and stream
+    waits, not in overlap.  The shard stays resident in HBM between the two
+    transfers (``device_buf``, or a fresh allocation of the shard's size)."""
     from . import scan as S
     n = xh.numel()
     if yh.numel() != n or xh.dtype != yh.dtype or xh.dim() != 1:
@@ -121,34 +118,14 @@ def sharded_scan_host(xh: torch.Tensor, yh: torch.Tensor, *, exclusive: bool = F
     if d.numel() < n or d.dtype != xh.dtype:
         raise ValueError("device_buf must hold the shard")
     d = d[:n]
-    nch = max(1, (n + chunk_elems - 1) // chunk_elems)
-    bounds = [(c * chunk_elems, min(n, (c + 1) * chunk_elems)) for c in range(nch)]
-    cur = torch.cuda.current_stream(dev)
-    s_in, s_comp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    s_in.wait_stream(cur)
-    s_comp.wait_stream(cur)
-    s_out.wait_stream(cur)
-    part = torch.empty(nch, dtype=xh.dtype, device=dev)
-    run = torch.empty(2, dtype=xh.dtype, device=dev)
-    for c, (lo, hi) in enumerate(bounds):
-        with torch.cuda.stream(s_in):
-            d[lo:hi].copy_(xh[lo:hi], non_blocking=True)
-        s_comp.wait_stream(s_in)
-        with torch.cuda.stream(s_comp):
-            S.reduce(d[lo:hi], part[c:c + 1], op=op)
-    with torch.cuda.stream(s_comp):
-        total = S.reduce(part, op=op)
-        totals = _gather_totals(total, world, group)
-        carry = S.carry_from_totals(totals, rank, op=op) if rank > 0 else None
-        fn = S.exclusive_scan if exclusive else S.inclusive_scan
-        for c, (lo, hi) in enumerate(bounds):
-            cin = carry if c == 0 else run[(c - 1) % 2:(c - 1) % 2 + 1]
-            fn(d[lo:hi], d[lo:hi], carry_in=cin, total_out=run[c % 2:c % 2 + 1], op=op)
-            s_out.wait_stream(s_comp)
-            with torch.cuda.stream(s_out):
-                yh[lo:hi].copy_(d[lo:hi], non_blocking=True)
-    s_out.synchronize()
-    cur.wait_stream(s_comp)
+    d.copy_(xh, non_blocking=True)
+    total = S.reduce(d, op=op)
+    totals = _gather_totals(total, world, group)
+    carry = S.carry_from_totals(totals, rank, op=op) if rank > 0 else None
+    fn = S.exclusive_scan if exclusive else S.inclusive_scan
+    fn(d, d, carry_in=carry, op=op)
+    yh.copy_(d, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
     return yh
 
 

@@ -135,3 +135,36 @@ def test_cyclic_scan_host_pipeline_world_one(S, oracle_lib):
                 sc.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_scan_host_world_one(S, oracle_lib):
+    # contiguous shards end to end from pinned host memory through
+    # torch.distributed (NCCL, world size 1): copy-in, reduce, all-gather,
+    # carried scan, copy-out — equals the oracle
+    import torch.distributed as dist
+
+    from paper_1604_04815_b200.distributed import sharded_scan_host
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        for tok in ("i32", "i64", "f64"):
+            n = 5_000_011
+            x = oracle_lib.generate_input(n, tok, [5, n])
+            xp = torch.from_numpy(x).pin_memory()
+            yp = torch.empty_like(xp).pin_memory()
+            sharded_scan_host(xp, yp)
+            ref = oracle_lib.c_sequential_scan(x)[0]
+            if tok[0] == "i":
+                assert np.array_equal(yp.numpy(), ref)
+            else:
+                assert oracle_lib.validate_output(x, yp.numpy(), ref=ref) is None
+            if tok == "i32":
+                buf = torch.empty(n + 7, dtype=xp.dtype, device="cuda")
+                sharded_scan_host(xp, yp, exclusive=True, op="max", device_buf=buf)
+                assert np.array_equal(yp.numpy(), oracle_lib.exclusive_scan(x, "max"))
+    finally:
+        dist.destroy_process_group()
