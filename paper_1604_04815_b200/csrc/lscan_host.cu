@@ -21,7 +21,6 @@
 #include <mutex>
 #include <string>
 #include <thread>
-#include <utility>
 #include <vector>
 
 #include "lscan.h"
@@ -34,46 +33,6 @@ namespace {
 
 constexpr int kBufs = 3;
 constexpr size_t kDefaultChunkMiB = 32;  // per-chunk bytes; LSCAN_HOST_CHUNK_MB overrides
-
-// LSCAN_HOST_RAMP=0: equal chunks only (lab A/B of the ramped schedule below)
-bool ramp_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("LSCAN_HOST_RAMP");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-// Chunk schedule (offset, length in elements): full chunks in the middle,
-// doubling from chunk/32 at the head and halving down to it at the tail.
-// The first copy-in runs alone (nothing to copy out yet) and the last
-// copy-out runs alone, so small end chunks shorten the time one PCIe
-// direction idles: with 32 MiB chunks, 2 x ~0.6 ms of a ~22 ms GiB pipeline.
-std::vector<std::pair<int64_t, int64_t>> chunk_schedule(int64_t n, int64_t chunk) {
-    std::vector<std::pair<int64_t, int64_t>> out;
-    std::vector<int64_t> ramp;  // chunk/32, chunk/16, ..., chunk/2
-    if (ramp_enabled())
-        for (int64_t c = std::max<int64_t>(chunk / 32, 1); c < chunk; c *= 2) ramp.push_back(c);
-    int64_t rsum = 0;
-    for (int64_t c : ramp) rsum += c;
-    int64_t off = 0;
-    auto push = [&](int64_t len) {
-        len = std::min(len, n - off);
-        if (len > 0) {
-            out.emplace_back(off, len);
-            off += len;
-        }
-    };
-    if (n <= 2 * rsum + chunk) {  // short arrays: equal chunks
-        while (off < n) push(chunk);
-        return out;
-    }
-    for (int64_t c : ramp) push(c);
-    while (n - off > rsum + chunk) push(chunk);
-    push(n - off - rsum);  // (0, chunk]
-    for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) push(*it);
-    return out;
-}
 
 size_t chunk_bytes_from_env() {
     const char *e = getenv("LSCAN_HOST_CHUNK_MB");
@@ -201,8 +160,7 @@ ls_status run_pipeline(HostCtx *c, ls_op op, ls_dtype dt, const void *x, void *y
     if (!direct && (st = ensure_staging(c)) != LS_OK) return st;
 
     const int64_t chunk = (int64_t)(c->chunk_bytes / es);
-    const std::vector<std::pair<int64_t, int64_t>> sched = chunk_schedule(n, chunk);
-    const int64_t nchunks = (int64_t)sched.size();
+    const int64_t nchunks = (n + chunk - 1) / chunk;
     const uint8_t *xb = static_cast<const uint8_t *>(x);
     uint8_t *yb = static_cast<uint8_t *>(y);
     uint8_t *carry = static_cast<uint8_t *>(c->carry);
@@ -210,7 +168,7 @@ ls_status run_pipeline(HostCtx *c, ls_op op, ls_dtype dt, const void *x, void *y
     auto drain = [&](int64_t k) -> ls_status {
         // finish chunk k on the host side (pageable path only)
         const int b = (int)(k % kBufs);
-        const int64_t off = sched[k].first, len = sched[k].second;
+        const int64_t off = k * chunk, len = std::min(chunk, n - off);
         HC(cudaEventSynchronize(c->ev_out[b]), "copy-out wait");
         parallel_memcpy(yb + off * es, c->pin_out[b], (size_t)len * es);
         return LS_OK;
@@ -218,7 +176,7 @@ ls_status run_pipeline(HostCtx *c, ls_op op, ls_dtype dt, const void *x, void *y
 
     for (int64_t k = 0; k < nchunks; ++k) {
         const int b = (int)(k % kBufs);
-        const int64_t off = sched[k].first, len = sched[k].second;
+        const int64_t off = k * chunk, len = std::min(chunk, n - off);
         const size_t bytes = (size_t)len * es;
         if (k >= kBufs) {
             // buffer b is free once chunk k - kBufs has left the device

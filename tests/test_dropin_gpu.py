@@ -163,11 +163,11 @@ def test_c8_throughput_over_sequential(oracle_lib):
 
 @pytest.mark.parametrize("tok", ["i32", "i64"])
 @pytest.mark.parametrize("pinned", [True, False])
-def test_ramped_chunk_schedule(oracle_lib, tok, pinned):
-    """The host pipeline's head / tail chunks ramp from chunk/32 up to the full
-    32 MiB chunk and back (lscan_host.cu chunk_schedule): exact across the
-    switch-over size (2 * ramp + chunk) and well past it, inclusive and
-    exclusive, pinned (direct DMA) and pageable (staged)."""
+def test_host_pipeline_chunk_counts(oracle_lib, tok, pinned):
+    """The host pipeline over 2-5 chunks of 32 MiB with ragged last chunks
+    (sizes from an A/B of ramped head / tail chunks, which measured equal to
+    equal chunks and was dropped): exact, inclusive and exclusive, pinned
+    (direct DMA) and pageable (staged)."""
     es = 4 if tok == "i32" else 8
     chunk = (32 << 20) // es
     ramp = sum(chunk >> s for s in range(1, 6))
