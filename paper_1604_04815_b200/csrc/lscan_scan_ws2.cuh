@@ -80,6 +80,10 @@ constexpr int kTimelineWords = 66;
 #define LS_WS2_PRED_SCAN 0
 #endif
 
+#ifndef LS_SHIFT_NAN_REDUCE
+#define LS_SHIFT_NAN_REDUCE 0
+#endif
+
 // f32 add on packed FADD2 (add.rn.f32x2, sm_100): the reducer folds two
 // elements per instruction (as IADD3 does for integers), and the scanners keep
 // each lane's running prefixes in place and add the row carry to two of them
@@ -242,6 +246,11 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
     constexpr int PER = 16 / (int)sizeof(T);
     constexpr int TILE_ELEMS = TILE_BYTES / (int)sizeof(T);
     static_assert(NV % 4 == 0, "a (half) tile must hold a multiple of 4 vectors per lane");
+    // lab (LS_SHIFT_NAN_REDUCE=1, with LS_SHIFT_RED2_32=0): f32 max / min over
+    // the window's elements [sh, sh + TILE_ELEMS) with FMNMX3.NAN, as the
+    // aligned reducer
+    if constexpr (LS_SHIFT_NAN_REDUCE && HALF < 0 && ScanFastOp<T, OP>::reduce_nan)
+        return reduce_stage_nan<T, OP, TILE_BYTES / 16 + 1>(st, lane, sh, sh + TILE_ELEMS);
     const T ident = OP::template identity<T>();
     T acc[4] = {ident, ident, ident, ident};
     const uint32_t base = smem_u32(st) + (HALF == 1 ? (uint32_t)TILE_BYTES / 2u : 0u) + (uint32_t)lane * 16;
