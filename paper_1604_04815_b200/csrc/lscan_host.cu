@@ -135,7 +135,9 @@ void parallel_memcpy(void *dst, const void *src, size_t bytes) {
         memcpy(dst, src, bytes);
         return;
     }
-    const size_t part = ((bytes / nt) + 4095) & ~(size_t)4095;
+    // ceil(bytes / nt) rounded up to a page: nt parts always cover every byte
+    // (floor(bytes / nt) already page-aligned would leave bytes % nt uncopied)
+    const size_t part = (((bytes + nt - 1) / nt) + 4095) & ~(size_t)4095;
     std::vector<std::thread> th;
     for (unsigned i = 1; i < nt; ++i) {
         const size_t off = part * i;

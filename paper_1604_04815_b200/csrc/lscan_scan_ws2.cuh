@@ -503,10 +503,16 @@ template <typename T, typename OP, bool MULTI, bool SHIFT>
 #ifndef LS_SHIFT_RED2_ADD
 #define LS_SHIFT_RED2_ADD 0
 #endif
+// LS_RED2_ADD (lab): the second reducer for add in the aligned kernel (the
+// single reducer publishes one 32 KiB tile per ~0.85 us at mid n)
+#ifndef LS_RED2_ADD
+#define LS_RED2_ADD 0
+#endif
 __host__ __device__ constexpr bool ws2_red2() {
     return !MULTI && (!SHIFT || LS_SHIFT_RED2) &&
            ((OP::idempotent && (sizeof(T) == 8 || (SHIFT && LS_SHIFT_RED2_32 && sizeof(T) == 4))) ||
-            (SHIFT && LS_SHIFT_RED2_ADD && !OP::idempotent && sizeof(T) == 8));
+            (SHIFT && LS_SHIFT_RED2_ADD && !OP::idempotent && sizeof(T) == 8) ||
+            (!SHIFT && LS_RED2_ADD && !OP::idempotent));
 }
 template <int SCAN_WARPS, bool MULTI, bool RED2>
 __host__ __device__ constexpr int ws2_threads_x() { return ws2_threads<SCAN_WARPS, MULTI>() + (RED2 ? 32 : 0); }

@@ -37,6 +37,7 @@ declare -A FLAGS=(
   [susp]="-DLS_LAB_SMALL=1 -DLS_MBAR_SUSPEND_NS=1000000"
   [wspred]="-DLS_LAB_SMALL=1 -DLS_WS2_PRED_SCAN=1"
   [shnan]="-DLS_LAB_SMALL=1 -DLS_SHIFT_NAN_REDUCE=1 -DLS_SHIFT_RED2_32=0"
+  [red2add]="-DLS_LAB_SMALL=1 -DLS_RED2_ADD=1"
   [srfla1]="-DLS_LAB_SMALL=1 -DLS_ROUND_FOLD=1 -DLS_FILL_LOOKAHEAD=1"
   [la1]="-DLS_FILL_LOOKAHEAD=1" [la2]="-DLS_FILL_LOOKAHEAD=2" [la3]="-DLS_FILL_LOOKAHEAD=3"
 )

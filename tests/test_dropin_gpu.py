@@ -186,3 +186,34 @@ def test_host_pipeline_chunk_counts(oracle_lib, tok, pinned):
         assert np.array_equal(y, oracle_lib.c_sequential_scan(x)[0]), (tok, n, pinned)
         ye = P.chained_exclusive_scan(P.ScanProblem(xs, op, out=ys))
         assert np.array_equal(ye, oracle_lib.c_sequential_scan(x, exclusive=True)[0]), (tok, n, pinned)
+
+
+@pytest.mark.parametrize("threads", [8, 16])
+def test_pageable_staging_copies_every_byte(threads):
+    """Pageable arrays are staged with a threaded host memcpy split into
+    page-rounded parts; chunks whose byte count is one element past a multiple
+    of threads x 4096 once lost their last element (the parts covered
+    threads x floor(bytes / threads)).  Run in a subprocess so the thread count
+    (read once per process) is the one under test."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    chunk = (32 << 20) // 4
+    n = 2 * chunk + threads * 1024 * 480 + 1   # last chunk: threads*4096*480 + 4 bytes
+    code = textwrap.dedent(f"""
+        import numpy as np, sys
+        sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+        import paper_1604_04815_b200 as P
+        x = (np.arange({n}, dtype=np.int64) % 1000 - 500).astype(np.int32)
+        y = P.chained_scan(P.ScanProblem(x, P.make_operator("add", "i32")))
+        ref = np.cumsum(x, dtype=np.int64).astype(np.int32)
+        assert np.array_equal(y, ref), int(np.nonzero(y != ref)[0][0])
+        buf = x.copy()
+        P.chained_scan(P.ScanProblem(buf, P.make_operator("add", "i32"), out=buf))
+        assert np.array_equal(buf, ref)
+        print("ok")
+    """)
+    env = dict(os.environ, LSCAN_HOST_COPY_THREADS=str(threads))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
