@@ -18,7 +18,9 @@ pytestmark = pytest.mark.gpu
 TDT = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32, "f64": torch.float64}
 
 SIZES = st.one_of(st.integers(1, 5000), st.integers(5000, 300_000), st.integers(300_000, 3_000_000),
-                  st.sampled_from([4096, 65536, 65537, 8192 * 148, 8192 * 148 + 1, (1 << 21) + 3]))
+                  st.sampled_from([4096, 65536, 65537, 8192 * 148, 8192 * 148 + 1, (1 << 21) + 3,
+                                   # the extra-large cluster geometry's range and just past it
+                                   3_500_001, 1 << 22, (1 << 22) + 1]))
 
 
 @pytest.fixture(scope="module")
@@ -69,3 +71,25 @@ def test_random_parity(S, oracle_lib, tok, op, excl, n, xoff, yoff, in_place, ca
             env = env[1:]
         err = np.abs(y.astype(np.float64) - ref.astype(np.float64))
         assert (err <= env + 1e-30).all(), what
+
+
+@settings(max_examples=16, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture, HealthCheck.too_slow])
+@given(tok=st.sampled_from(["i32", "i64"]), op=st.sampled_from(["add", "max"]), excl=st.booleans(),
+       n=st.one_of(st.integers(1, 3_000_000), st.integers(8_000_000, 30_000_000)),
+       pinned=st.booleans(), seed=st.integers(0, 2**31))
+def test_random_host_pipeline(oracle_lib, tok, op, excl, n, pinned, seed):
+    """The numpy drop-in's host pipeline (32 MiB device chunks, pinned DMA or
+    pageable staging through the threaded memcpy) at random sizes: exact."""
+    import paper_1604_04815_b200 as P
+    x = oracle_lib.generate_input(n, tok, [seed, n])
+    if pinned:
+        xp = torch.from_numpy(x).pin_memory()
+        yp = torch.empty_like(xp).pin_memory()
+        xs, ys = xp.numpy(), yp.numpy()
+    else:
+        xs, ys = x, np.empty_like(x)
+    prob = P.ScanProblem(xs, P.make_operator(op, tok), out=ys)
+    y = P.chained_exclusive_scan(prob) if excl else P.chained_scan(prob)
+    ref = oracle_lib.exclusive_scan(x, op) if excl else oracle_lib.sequential_scan(x, op=op)
+    assert np.array_equal(y, ref), (tok, op, excl, n, pinned)
