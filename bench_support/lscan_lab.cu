@@ -28,7 +28,7 @@ template <typename T, typename OP, int SW, int TILE, int STAGES, int VW, bool SH
 LabK labk() {
     constexpr bool R2 = ws2_red2<T, OP, false, SHIFT>();
     return {&scan_ws2_kernel<T, OP, SW, TILE, STAGES, false, false, SHIFT, VW>, ws2_threads_x<SW, false, R2>(),
-            scan_ws2_smem_bytes<T, SW, TILE, STAGES, SHIFT, R2>()};
+            scan_ws2_smem_bytes<T, SW, TILE, STAGES, SHIFT, R2, lscan::row_transpose<T, OP>()>()};
 }
 
 template <typename T, typename OP, int SW, int TILE, int STAGES, int VW>

@@ -494,25 +494,58 @@ struct ScanFastOp<float, struct OpMin> {
 #ifndef LS_F64_FAST_SCAN
 #define LS_F64_FAST_SCAN 0
 #endif
-#if LS_F64_FAST_SCAN
+// f64 NaN-free scans (LS_F64_NANFREE_SCAN): on operands that are not NaN,
+// numpy's maximum(a, b) is exactly (a > b) ? a : b — equal operands (+-0
+// included) give the right one — so a chunk without NaNs scans with one
+// DSETP and two selects per operator and a two-deep dependency chain instead
+// of the exact form's NaN test, ordered test and selects.  The chunk test is
+// one FADD per element on the high words viewed as f32 (a f64 NaN or infinity
+// has all of f32's exponent bits set there, so their sum is not finite)
+#ifndef LS_F64_NANFREE_SCAN
+#define LS_F64_NANFREE_SCAN 0
+#endif
+template <bool GT>
+struct OpNanFreeD {
+    static constexpr int code = GT ? 1 : 2;
+    static constexpr bool idempotent = true;
+    static constexpr bool three = false;
+    __device__ __forceinline__ static double apply(double a, double b) {
+        double r;
+        if constexpr (GT)
+            asm("{\n .reg .pred p;\n setp.gt.f64 p, %1, %2;\n selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(a), "d"(b));
+        else
+            asm("{\n .reg .pred p;\n setp.lt.f64 p, %1, %2;\n selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(a), "d"(b));
+        return r;
+    }
+};
+#if LS_F64_FAST_SCAN || LS_F64_NANFREE_SCAN
 template <>
 struct ScanFastOp<double, struct OpMax> {
     static constexpr bool enabled = true;
     static constexpr bool reduce_nan = false;
+#if LS_F64_NANFREE_SCAN
+    using type = OpNanFreeD<true>;
+#else
     using type = OpFastMaxD;
+#endif
 };
 template <>
 struct ScanFastOp<double, struct OpMin> {
     static constexpr bool enabled = true;
     static constexpr bool reduce_nan = false;
+#if LS_F64_NANFREE_SCAN
+    using type = OpNanFreeD<false>;
+#else
     using type = OpFastMinD;
+#endif
 };
 #endif
 
 // A lane's registers hold no zero and no NaN (the fast operators' domain).
 // 32-bit words: u = 2 * bits - 1 is 0xffffffff for +-0 and above 0xff000000
 // for a NaN, at most 0xfeffffff otherwise (infinities included); 64-bit
-// elements the same on the doubled bit pattern (NaN above 0xffe0...0)
+// elements the same on the doubled bit pattern (NaN above 0xffe0...0), or,
+// for the NaN-free f64 operators, no NaN and no infinity
 template <typename T, int V>
 __device__ __forceinline__ bool fast_domain(const uint4 (&q)[V]) {
     if constexpr (sizeof(T) == 4) {
@@ -523,6 +556,15 @@ __device__ __forceinline__ bool fast_domain(const uint4 (&q)[V]) {
             mx1 = max(mx1, max(q[i].z + q[i].z - 1u, q[i].w + q[i].w - 1u));
         }
         return max(mx0, mx1) <= 0xff000000u;
+    } else if (LS_F64_NANFREE_SCAN) {
+        // no NaN (nor infinity): the high words' f32 sum stays finite
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            s0 += __uint_as_float(q[i].y);
+            s1 += __uint_as_float(q[i].w);
+        }
+        return fabsf(s0 + s1) < INFINITY;
     } else {
         unsigned long long mx = 0ull;
 #pragma unroll

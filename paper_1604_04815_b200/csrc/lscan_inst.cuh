@@ -26,7 +26,7 @@ Launch fast_launch() {
     constexpr bool R2 = ws2_red2<T, OP, false, false>();
     return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, false, ws2_vw<T, OP>()>,
             ws2_threads_x<C::kScanWarps, false, R2>(),
-            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, false, R2>(), C::kTileBytes, C::kStages};
+            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, false, R2, row_transpose<T, OP>()>(), C::kTileBytes, C::kStages};
 }
 
 // the shifted-window kernel's rows: 16-byte for 32-bit add (785 vs 733
@@ -43,7 +43,7 @@ Launch shift_launch() {
     constexpr bool R2 = ws2_red2<T, OP, false, true>();
     return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, false, true, shift_vw<T, OP>()>,
             ws2_threads_x<C::kScanWarps, false, R2>(),
-            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true, R2>(), C::kTileBytes, C::kStages};
+            scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, true, R2, row_transpose<T, OP>()>(), C::kTileBytes, C::kStages};
 }
 
 template <typename T, typename OP, bool EXCL>
@@ -55,7 +55,7 @@ Launch multi_launch() {
     // live (16-byte rows spilled 12 bytes in the i64 instantiations)
     constexpr int VW = sizeof(T) == 8 ? 2 : 1;
     return {&scan_ws2_kernel<T, OP, C::kScanWarps, C::kTileBytes, C::kStages, EXCL, true, false, VW>,
-            ws2_threads<C::kScanWarps, true>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages>(),
+            ws2_threads<C::kScanWarps, true>(), scan_ws2_smem_bytes<T, C::kScanWarps, C::kTileBytes, C::kStages, false, false, row_transpose<T, OP>()>(),
             C::kTileBytes, C::kStages};
 }
 

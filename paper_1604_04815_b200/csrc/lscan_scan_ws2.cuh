@@ -120,6 +120,36 @@ __host__ __device__ constexpr bool packed_f32_add() {
     return LS_F32_PACKED && std::is_same<T, float>::value && OP::code == 0 && !OP::idempotent;
 }
 
+// 64-bit max / min: the scanners keep each lane's in-lane running prefixes
+// in place (the row fold's intermediates), so the store pass combines the
+// carry with every element independently instead of re-folding the lane's
+// chunk serially (the exact f64 operator is a three-deep chain per element)
+#ifndef LS_PIP_MAXMIN
+#define LS_PIP_MAXMIN 0
+#endif
+template <typename T, typename OP>
+__host__ __device__ constexpr bool pip_maxmin() {
+    return LS_PIP_MAXMIN && sizeof(T) == 8 && OP::code != 0;
+}
+
+// Transposed row scan (TRS): a scanner lane's VR row totals are written to a
+// per-warp scratch in sequence order (row-major over lanes), each lane reads
+// back VR consecutive ones, folds them, and ONE warp scan plus one exclusive
+// shuffle gives every (row, lane) its exclusive prefix over all rows and lanes
+// before it — instead of VR warp scans, VR shuffles of the row totals and a
+// serial carry over rows.  Sequence order is kept throughout (left operand =
+// earlier elements), so it is exact for the order-sensitive float max / min.
+// LS_ROW_TRANSPOSE: 0 off, 1 order-sensitive 64-bit ops (f64 max / min),
+// 2 every 64-bit max / min, 3 every operator and type
+#ifndef LS_ROW_TRANSPOSE
+#define LS_ROW_TRANSPOSE 1
+#endif
+template <typename T, typename OP>
+__host__ __device__ constexpr bool row_transpose() {
+    return (LS_ROW_TRANSPOSE == 1 && sizeof(T) == 8 && order_sensitive<T, OP>()) ||
+           (LS_ROW_TRANSPOSE == 2 && sizeof(T) == 8 && OP::code != 0) || LS_ROW_TRANSPOSE == 3;
+}
+
 __device__ __forceinline__ void stg128(void *p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
@@ -568,6 +598,8 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
     T *warp_exc = warp_tot + SCAN_WARPS;
     uint64_t *red2_ready = reinterpret_cast<uint64_t *>(warp_exc + SCAN_WARPS);  // RED2: upper half reduced
     T *red2_val = reinterpret_cast<T *>(red2_ready + STAGES);
+    // TRS scratch: V * 32 values per scanner warp, 16-byte aligned
+    T *trs_base = reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(red2_val + STAGES) + 15u) & ~(uintptr_t)15u);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
@@ -998,12 +1030,62 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             // place (the fold's intermediates), so the carry is added to every
             // element independently, two per FADD2, once the prefix is known
             constexpr bool PIP = packed_f32_add<T, OP>() && !EXCL;
+            constexpr bool PIPM = pip_maxmin<T, OP>();
+            // TRS: rex[j] is this lane's exclusive prefix over the rows before
+            // j and the lanes before it in row j (undefined at row 0, lane 0)
+            constexpr bool TRS = row_transpose<T, OP>() && VR > 1 && !PIP && !LS_LAB_SKIP_ROWSCAN;
             auto row_scans = [&](auto opv) {
                 using O = decltype(opv);
+                if constexpr (TRS) {
+                    T *trs = trs_base + warp * (V * 32);
+#pragma unroll
+                    for (int j = 0; j < VR; ++j) {
+                        T v = r.e[j * RPER];
+                        if constexpr (PIPM) {
+#pragma unroll
+                            for (int e = 1; e < RPER; ++e) r.e[j * RPER + e] = v = O::apply(v, r.e[j * RPER + e]);
+                        } else if constexpr (O::three) {
+#pragma unroll
+                            for (int e = 1; e + 1 < RPER; e += 2) v = O::apply3(v, r.e[j * RPER + e], r.e[j * RPER + e + 1]);
+                            if constexpr (RPER % 2 == 0) v = O::apply(v, r.e[j * RPER + RPER - 1]);
+                        } else {
+#pragma unroll
+                            for (int e = 1; e < RPER; ++e) v = O::apply(v, r.e[j * RPER + e]);
+                        }
+                        trs[j * 32 + lane] = v;
+                    }
+                    __syncwarp();
+                    T f[VR];  // in-lane inclusive prefixes of values VR*lane .. VR*lane + VR - 1
+                    if constexpr (VR % 2 == 0 && sizeof(T) == 8) {
+#pragma unroll
+                        for (int i = 0; i < VR; i += 2) {
+                            const uint4 w = lds128(smem_u32(trs + VR * lane + i));
+                            const uint64_t a = ((uint64_t)w.y << 32) | w.x, b = ((uint64_t)w.w << 32) | w.z;
+                            memcpy(&f[i], &a, 8);
+                            memcpy(&f[i + 1], &b, 8);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < VR; ++i) f[i] = trs[VR * lane + i];
+                    }
+#pragma unroll
+                    for (int i = 1; i < VR; ++i) f[i] = O::apply(f[i - 1], f[i]);
+                    const T inc = warp_inclusive_scan<T, O, LS_WS2_PRED_SCAN != 0>(f[VR - 1], lane);
+                    const T exl = __shfl_up_sync(0xffffffffu, inc, 1);
+                    run = __shfl_sync(0xffffffffu, inc, 31);
+                    // exclusive prefix of value VR*lane + i: lanes' values before,
+                    // then this lane's first i (lane 0, i = 0: none, left as is)
+                    if (lane > 0) trs[VR * lane] = exl;
+#pragma unroll
+                    for (int i = 1; i < VR; ++i) trs[VR * lane + i] = lane > 0 ? O::apply(exl, f[i - 1]) : f[i - 1];
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < VR; ++j) rex[j] = trs[j * 32 + lane];
+                } else {
 #pragma unroll
                 for (int j = 0; j < VR; ++j) {
                     T v = r.e[j * RPER];
-                    if constexpr (PIP) {
+                    if constexpr (PIP || PIPM) {
 #pragma unroll
                         for (int e = 1; e < RPER; ++e) r.e[j * RPER + e] = v = O::apply(v, r.e[j * RPER + e]);
                     } else if constexpr (O::three) {
@@ -1034,6 +1116,7 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                 run = rtot[0];
 #pragma unroll
                 for (int j = 1; j < VR; ++j) run = O::apply(run, rtot[j]);
+                }
             };
             if constexpr (ScanFastOp<T, OP>::enabled) {
                 if (fast) row_scans(typename ScanFastOp<T, OP>::type{});
@@ -1074,7 +1157,8 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
             // the warp total above; no per-row array kept across the wait)
             auto fold_store = [&](auto opv, bool nan_fill) {
                 using O = decltype(opv);
-                T rowpre = rtot[0];
+                [[maybe_unused]] T rowpre = ident;
+                if constexpr (!TRS) rowpre = rtot[0];
 #pragma unroll
                 for (int j = 0; j < VR; ++j) {
                     if (nan_fill) {
@@ -1085,12 +1169,16 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                     } else {
                         bool has = has0;
                         T acc = wcarry;
+                        if constexpr (TRS) {
+                            if (j > 0 || lane > 0) { acc = has ? O::apply(acc, rex[j]) : rex[j]; has = true; }
+                        } else {
                         if (j > 0) {
                             acc = has ? O::apply(acc, rowpre) : rowpre;
                             has = true;
                             if (j + 1 < VR) rowpre = O::apply(rowpre, rtot[j]);
                         }
                         if (lane > 0) { acc = has ? O::apply(acc, rex[j]) : rex[j]; has = true; }
+                        }
                         if constexpr (PIP) {
                             // y = carry (+) in-lane prefix; nothing to add before the
                             // array's first element (no carry: y[0] = x[0] exactly)
@@ -1102,6 +1190,18 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
                                     unpack2(fadd2(cc, pack2(w.x, w.y)), w.x, w.y);
                                     unpack2(fadd2(cc, pack2(w.z, w.w)), w.z, w.w);
                                 }
+                            }
+                        } else if constexpr (PIPM) {
+                            // y_e = carry (+) p_e (exclusive: carry (+) p_{e-1}),
+                            // every element independent of the others
+                            if constexpr (EXCL) {
+#pragma unroll
+                                for (int e = RPER - 1; e > 0; --e)
+                                    r.e[j * RPER + e] = has ? O::apply(acc, r.e[j * RPER + e - 1]) : r.e[j * RPER + e - 1];
+                                r.e[j * RPER] = has ? acc : ident;
+                            } else if (has) {
+#pragma unroll
+                                for (int e = 0; e < RPER; ++e) r.e[j * RPER + e] = O::apply(acc, r.e[j * RPER + e]);
                             }
                         } else {
 #pragma unroll
@@ -1202,10 +1302,13 @@ __global__ void __launch_bounds__(ws2_threads_x<SCAN_WARPS, MULTI, ws2_red2<T, O
     }
 }
 
-template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool SHIFT = false, bool RED2 = false>
+template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool SHIFT = false, bool RED2 = false,
+          bool TRS = false>
 constexpr size_t scan_ws2_smem_bytes() {
     return (size_t)STAGES * (TILE_BYTES + (SHIFT ? 16 : 0)) + 4 * STAGES * 8 + STAGES * sizeof(T) +
-           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32 + (RED2 ? STAGES * (8 + sizeof(T)) : 0);
+           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32 + (RED2 || LS_ROW_TRANSPOSE ? STAGES * (8 + sizeof(T)) : 0) +
+           // TRS scratch (after the RED2 region) (row_transpose): V * 32 values per scanner warp + alignment
+           (LS_ROW_TRANSPOSE ? 16 + (size_t)TILE_BYTES / 16 * sizeof(T) : 0);
 }
 
 }  // namespace lscan

@@ -14,6 +14,10 @@
 #   evictnormal  evict-normal L2 policy on the TMA loads
 #   nopack       f32 add without the packed FADD2 forms (LS_F32_PACKED=0)
 #   f64fast      f64 max/min fast scans on chunks without zeros or NaNs
+#   f64nanfree   f64 max/min (a > b) ? a : b scans on chunks without NaNs
+#   trs1/2/3     transposed row scans (LS_ROW_TRANSPOSE) for f64 max/min / 64-bit max/min / everything
+#   pipmm        64-bit max/min keep in-lane prefixes in place (LS_PIP_MAXMIN)
+#   pipmmnf      pipmm + f64nanfree
 #   timeline     per-CTA event times (LS_LAB_TIMELINE; production geometries only)
 #   small        production geometries only (cfgs 60, 61, 65)
 #   sla1/2/3     small + look-ahead 1/2/3
@@ -26,7 +30,10 @@ declare -A FLAGS=(
   [skipboth]="-DLS_LAB_SKIP_REDUCE=1 -DLS_LAB_SKIP_ROWSCAN=1" [skiplb]="-DLS_LAB_SKIP_LOOKBACK=1"
   [timing]="-DLS_LAB_TIMING=1" [sleep200]="-DLS_LOOKBACK_SLEEP_NS=200" [sleep1000]="-DLS_LOOKBACK_SLEEP_NS=1000"
   [evictnormal]="-DLS_TMA_EVICT_FIRST=0" [nopack]="-DLS_F32_PACKED=0"
-  [f64fast]="-DLS_F64_FAST_SCAN=1"
+  [f64fast]="-DLS_F64_FAST_SCAN=1" [f64nanfree]="-DLS_F64_NANFREE_SCAN=1"
+  [trs1]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=1" [trs2]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=2"
+  [trs3]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=3"
+  [pipmm]="-DLS_PIP_MAXMIN=1" [pipmmnf]="-DLS_PIP_MAXMIN=1 -DLS_F64_NANFREE_SCAN=1"
   [timeline]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1" [small]="-DLS_LAB_SMALL=1"
   [tlrfold]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_ROUND_FOLD=1" [tlla1]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_FILL_LOOKAHEAD=1"
   [sla1]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=1" [sla2]="-DLS_LAB_SMALL=1 -DLS_FILL_LOOKAHEAD=2"
