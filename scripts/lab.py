@@ -87,6 +87,8 @@ def main():
                     help="shifted-window kernel: x one element past a 16-byte boundary, y aligned")
     ap.add_argument("--sustain", type=int, default=0,
                     help="report this many consecutive blocks of --reps calls per config (drift under load)")
+    ap.add_argument("--data", choices=["random", "ascending"], default="random",
+                    help="ascending: sorted increasing input (a running max never keeps its carry)")
     args = ap.parse_args()
     L = N.lib()
     LAB = ctypes.CDLL(os.path.join(REPO, "bench_support", "_build", args.labso))
@@ -103,6 +105,8 @@ def main():
         x = torch.rand(m, dtype=dt, device="cuda") * 2 - 1
     else:
         x = torch.randint(-2**31, 2**31 - 1, (m,), dtype=dt, device="cuda")
+    if args.data == "ascending":
+        x = torch.sort(x).values
     if args.shift:
         x = x[1:]  # 4 or 8 bytes past the allocation's (256-byte) alignment
     y = torch.empty_like(x)
