@@ -1306,9 +1306,9 @@ template <typename T, int SCAN_WARPS, int TILE_BYTES, int STAGES, bool SHIFT = f
           bool TRS = false>
 constexpr size_t scan_ws2_smem_bytes() {
     return (size_t)STAGES * (TILE_BYTES + (SHIFT ? 16 : 0)) + 4 * STAGES * 8 + STAGES * sizeof(T) +
-           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32 + (RED2 || LS_ROW_TRANSPOSE ? STAGES * (8 + sizeof(T)) : 0) +
-           // TRS scratch (after the RED2 region) (row_transpose): V * 32 values per scanner warp + alignment
-           (LS_ROW_TRANSPOSE ? 16 + (size_t)TILE_BYTES / 16 * sizeof(T) : 0);
+           (STAGES + 1) * 4 + 2 * SCAN_WARPS * sizeof(T) + 32 + (RED2 || TRS ? STAGES * (8 + sizeof(T)) : 0) +
+           // TRS scratch (row_transpose<T, OP>(), after the RED2 region): V * 32 values per scanner warp
+           (TRS ? 16 + (size_t)TILE_BYTES / 16 * sizeof(T) : 0);
 }
 
 }  // namespace lscan
