@@ -219,6 +219,9 @@ __device__ __forceinline__ T reduce_stage_nan(const uint8_t *st, int lane, int l
     return x;
 }
 
+#ifndef LS_F64_FAST_REDUCE
+#define LS_F64_FAST_REDUCE 1
+#endif
 template <typename T, typename OP, int TILE_BYTES>
 __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
     constexpr int NV = TILE_BYTES / 16 / 32;  // 16-byte vectors per lane
@@ -247,6 +250,36 @@ __device__ __forceinline__ T reduce_stage(const uint8_t *st, int lane) {
         return warp_reduce_fixed<T, OP>(__uint_as_float(lo) + __uint_as_float(hi));
     }
     const T ident = OP::template identity<T>();
+    if constexpr (LS_F64_FAST_REDUCE && std::is_same<T, double>::value && OP::code != 0) {
+        // f64 max / min: order-free max.f64 / min.f64 (one DSETP.MAX + selects;
+        // drops NaNs, either zero on a tie) beside a NaN screen — the high
+        // words viewed as f32 through the NaN-propagating FMNMX3 (an f64 NaN or
+        // infinity is an f32 NaN there).  A flagged tile (NaN, infinity or a
+        // magnitude >= 2^1017) is folded again exactly; a zero result is
+        // re-derived by tile_ties as before
+        using F = typename std::conditional<OP::code == 1, OpFastMaxD, OpFastMinD>::type;
+        double fa[4] = {ident, ident, ident, ident};
+        float nf = 0.f;
+        const uint32_t fbase = smem_u32(st) + (uint32_t)lane * 16;
+#pragma unroll 2
+        for (int j = 0; j < NV; j += 4) {
+            Regs<T, 4> r;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) r.q[u] = lds128(fbase + (uint32_t)(j + u) * 512u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                fa[u] = F::apply(F::apply(fa[u], r.e[u * 2]), r.e[u * 2 + 1]);
+                nf = OpNanMaxF::apply3(nf, __uint_as_float(r.q[u].y), __uint_as_float(r.q[u].w));
+            }
+        }
+        if (!__any_sync(0xffffffffu, nf != nf)) {
+            double a = F::apply(F::apply(fa[0], fa[1]), F::apply(fa[2], fa[3]));
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) a = F::apply(a, __shfl_xor_sync(0xffffffffu, a, d));
+            if (a == 0.0) return tile_ties<T, OP>(st, lane, a, TILE_BYTES / 16, 0, TILE_BYTES / (int)sizeof(T));
+            return a;
+        }
+    }
     T acc[4] = {ident, ident, ident, ident};
     const uint32_t base = smem_u32(st) + (uint32_t)lane * 16;
 #pragma unroll 2

@@ -16,6 +16,7 @@
 #   f64fast      f64 max/min fast scans on chunks without zeros or NaNs
 #   f64nanfree   f64 max/min (a > b) ? a : b scans on chunks without NaNs
 #   trs1/2/3     transposed row scans (LS_ROW_TRANSPOSE) for f64 max/min / 64-bit max/min / everything
+#   f64red       f64 max/min reducers: order-free max.f64 + f32-view NaN screen (LS_F64_FAST_REDUCE)
 #   pipmm        64-bit max/min keep in-lane prefixes in place (LS_PIP_MAXMIN)
 #   pipmmnf      pipmm + f64nanfree
 #   timeline     per-CTA event times (LS_LAB_TIMELINE; production geometries only)
@@ -33,6 +34,7 @@ declare -A FLAGS=(
   [f64fast]="-DLS_F64_FAST_SCAN=1" [f64nanfree]="-DLS_F64_NANFREE_SCAN=1"
   [trs1]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=1" [trs2]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=2"
   [trs3]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=3"
+  [f64red]="-DLS_LAB_SMALL=1 -DLS_F64_FAST_REDUCE=1"
   [pipmm]="-DLS_PIP_MAXMIN=1" [pipmmnf]="-DLS_PIP_MAXMIN=1 -DLS_F64_NANFREE_SCAN=1"
   [timeline]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1" [small]="-DLS_LAB_SMALL=1"
   [tlrfold]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_ROUND_FOLD=1" [tlla1]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_FILL_LOOKAHEAD=1"

@@ -47,6 +47,13 @@ def make(kind, tok, op, n, seed):
         k = max(1, n // 20000)
         pos = rng.choice(n, size=min(n, 4 * k), replace=False)
         x[pos] = np.where(rng.random(pos.size) < 0.5, dt(-0.0), dt(0.0))
+    elif kind == "extremes":       # infinities, magnitudes >= 2^1017 (f64) / near FLT_MAX and zeros
+        x = rng.uniform(-1, 1, n).astype(dt)   # in a few tiles: the reducers' NaN screen flags
+        big = np.array([np.inf, -np.inf, 2.0 ** 1020, -(2.0 ** 1020), 2.0 ** 1017, 0.0, -0.0]
+                       if tok == "f64" else [np.inf, -np.inf, 3.0e38, -3.0e38, 0.0, -0.0])
+        k = max(1, n // 50000)
+        pos = rng.choice(n, size=min(n, 3 * k), replace=False)
+        x[pos] = big[rng.integers(0, big.size, pos.size)].astype(dt)
     else:                          # "nans": several NaN payloads clustered in one region
         x = rng.uniform(-1, 1, n).astype(dt)
         lo = rng.integers(0, max(1, n - 4096))
@@ -62,7 +69,7 @@ def seq(x, op):
 
 @pytest.mark.parametrize("tok", ["f32", "f64"])
 @pytest.mark.parametrize("op", ["max", "min"])
-@pytest.mark.parametrize("kind", ["dense_zeros", "sparse_zeros", "nans"])
+@pytest.mark.parametrize("kind", ["dense_zeros", "sparse_zeros", "nans", "extremes"])
 @pytest.mark.parametrize("n,path", [(3000, "auto"), (300_000, "auto"), (300_000, "cluster"),
                                     ((1 << 22) + 5, "persistent"), ((1 << 22) + 5, "auto")])
 @pytest.mark.parametrize("excl", [False, True])
