@@ -24,10 +24,13 @@ struct LabK {
     size_t smem;
 };
 
+#ifndef LS_LAB_EXCL
+#define LS_LAB_EXCL 0  // 1: exclusive scans (timing only: lab.py checks inclusive results)
+#endif
 template <typename T, typename OP, int SW, int TILE, int STAGES, int VW, bool SHIFT>
 LabK labk() {
     constexpr bool R2 = ws2_red2<T, OP, false, SHIFT>();
-    return {&scan_ws2_kernel<T, OP, SW, TILE, STAGES, false, false, SHIFT, VW>, ws2_threads_x<SW, false, R2>(),
+    return {&scan_ws2_kernel<T, OP, SW, TILE, STAGES, LS_LAB_EXCL != 0, false, SHIFT, VW>, ws2_threads_x<SW, false, R2>(),
             scan_ws2_smem_bytes<T, SW, TILE, STAGES, SHIFT, R2, lscan::row_transpose<T, OP>()>()};
 }
 

@@ -17,6 +17,8 @@
 #   f64nanfree   f64 max/min (a > b) ? a : b scans on chunks without NaNs
 #   trs1/2/3     transposed row scans (LS_ROW_TRANSPOSE) for f64 max/min / 64-bit max/min / everything
 #   f64red       f64 max/min reducers: order-free max.f64 + f32-view NaN screen (LS_F64_FAST_REDUCE)
+#   excl / exclpipm / inclpipm   exclusive scans (timing only) without / with in-place
+#                prefixes (LS_PIP_MAXMIN), inclusive with them
 #   pipmm        64-bit max/min keep in-lane prefixes in place (LS_PIP_MAXMIN)
 #   pipmmnf      pipmm + f64nanfree
 #   timeline     per-CTA event times (LS_LAB_TIMELINE; production geometries only)
@@ -35,6 +37,8 @@ declare -A FLAGS=(
   [trs1]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=1" [trs2]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=2"
   [trs3]="-DLS_LAB_SMALL=1 -DLS_ROW_TRANSPOSE=3"
   [f64red]="-DLS_LAB_SMALL=1 -DLS_F64_FAST_REDUCE=1"
+  [excl]="-DLS_LAB_SMALL=1 -DLS_LAB_EXCL=1" [exclpipm]="-DLS_LAB_SMALL=1 -DLS_LAB_EXCL=1 -DLS_PIP_MAXMIN=1"
+  [inclpipm]="-DLS_LAB_SMALL=1 -DLS_PIP_MAXMIN=1"
   [pipmm]="-DLS_PIP_MAXMIN=1" [pipmmnf]="-DLS_PIP_MAXMIN=1 -DLS_F64_NANFREE_SCAN=1"
   [timeline]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1" [small]="-DLS_LAB_SMALL=1"
   [tlrfold]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_ROUND_FOLD=1" [tlla1]="-DLS_LAB_SMALL=1 -DLS_LAB_TIMELINE=1 -DLS_FILL_LOOKAHEAD=1"
