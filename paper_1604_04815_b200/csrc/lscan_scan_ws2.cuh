@@ -315,6 +315,8 @@ __device__ __forceinline__ T reduce_stage_shifted(const uint8_t *st, int lane, i
     if constexpr (LS_SHIFT_NAN_REDUCE && HALF < 0 && ScanFastOp<T, OP>::reduce_nan)
         return reduce_stage_nan<T, OP, TILE_BYTES / 16 + 1>(st, lane, sh, sh + TILE_ELEMS);
     const T ident = OP::template identity<T>();
+    // (the aligned reducer's order-free f64 form measured slower here: shifted
+    // f64 max 355 -> 342 Gelem/s, profiles/r2_f64_maxmin_ab.json)
     T acc[4] = {ident, ident, ident, ident};
     const uint32_t base = smem_u32(st) + (HALF == 1 ? (uint32_t)TILE_BYTES / 2u : 0u) + (uint32_t)lane * 16;
 #pragma unroll 2

@@ -112,7 +112,7 @@ def test_ties_reduce(S, tok, op, kind, n):
 
 @pytest.mark.parametrize("tok", ["f32", "f64"])
 @pytest.mark.parametrize("op", ["max", "min"])
-@pytest.mark.parametrize("kind", ["dense_zeros", "sparse_zeros", "nans"])
+@pytest.mark.parametrize("kind", ["dense_zeros", "sparse_zeros", "nans", "extremes"])
 @pytest.mark.parametrize("xoff,yoff", [(1, 0), (0, 1), (3, 2)])
 def test_ties_misaligned(S, tok, op, kind, xoff, yoff):
     """x and y misaligned differently: one launch — y's head folded into the
