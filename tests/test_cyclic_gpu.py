@@ -255,3 +255,37 @@ def test_back_to_back_calls_of_unequal_length(env, oracle_lib):
             assert np.array_equal(y, oracle_lib.sequential_scan(glob, op=("add", "max")[i % 2])), (i, n)
     finally:
         v.close()
+
+
+@pytest.mark.parametrize("op", ["max", "min"])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_virtual_gpus_f64_maxmin_ties(env, op, exclusive):
+    """The fused block-cyclic kernel's f64 max/min (transposed row scans,
+    order-free reducers with the NaN screen) on data with signed zeros,
+    NaN payloads and infinities: raw bits against numpy's sequential fold."""
+    N, S, _ = env
+    W = 2
+    tile = S.query_multi_config(torch.float64, 1 << 20)["tile_elems"]
+    grid = S.query_config(torch.float64, 1 << 20)["sms"] // W
+    stripe = grid * tile
+    n = 3 * stripe + 2 * tile + 45
+    rng = np.random.default_rng([11, n])
+    sign = -1.0 if op == "max" else 1.0
+    parts = []
+    for g in range(W):
+        x = sign * rng.random(n)
+        pos = rng.choice(n, size=40, replace=False)
+        x[pos[:30]] = np.where(rng.random(30) < 0.5, -0.0, 0.0)
+        x[pos[30:35]] = np.array([np.inf, -np.inf, 2.0 ** 1020, -(2.0 ** 1020), 0.0])
+        if g == 1:  # NaNs with payloads late in the second GPU's data
+            x[pos[35:]] = np.array([0x7FF8000000000123, 0xFFF800000000BEEF, 0x7FF8000000000000,
+                                    0xFFF8000000000000, 0x7FF8000000000777], np.uint64).view(np.float64)
+        parts.append(x)
+    xd = [torch.from_numpy(p).cuda() for p in parts]
+    outs, _, _ = run_virtual(env, xd, op=op, exclusive=exclusive)
+    glob = assemble(parts, stripe)
+    y = assemble([o.cpu().numpy() for o in outs], stripe)
+    inc = (np.maximum if op == "max" else np.minimum).accumulate(glob)
+    ref = np.concatenate([[-np.inf if op == "max" else np.inf], inc[:-1]]) if exclusive else inc
+    bad = np.flatnonzero(y.view(np.uint64) != ref.view(np.uint64))
+    assert bad.size == 0, f"{bad.size} mismatching bits, first at {bad[:5]}"
